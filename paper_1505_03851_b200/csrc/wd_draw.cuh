@@ -1,0 +1,413 @@
+// wd_draw.cuh -- the draw kernels (butterfly and prefix-table) for sm_100a.
+//
+// Reference behaviour (paths under /root/reference/pkg/src/warpdraw/):
+//   kernels.py:170-225  build_butterfly_table   -> bfly_kernel pass 1
+//   kernels.py:268-362  butterfly_search / walk -> bfly_kernel pass 2
+//   kernels.py:95-101   _stops_from_units       -> make_stop
+//   kernels.py:487-539  draw_z_butterfly        -> bfly_kernel<..., LDA>
+//   kernels.py:580-600  build_block_tables      -> bfly_kernel<..., ROWS>
+//   kernels.py:380-484  draw_z_basic/transposed -> prefix_kernel
+//
+// Layout and mapping:
+//   * one warp owns a CHUNK of 32 consecutive tokens (CSR order) or rows;
+//   * the block loop walks W-topic blocks; per block every lane issues L
+//     vector loads, each covering E consecutive topics of one row, so a warp
+//     instruction reads R full contiguous row segments of W*sizeof(T) bytes
+//     (128 B for fp32, W=32): coalesced and 128-bit vectorised;
+//   * the first log2(E) levels of each block's pairwise tree are summed in
+//     registers, the remaining log2(L) levels by a transpose-reduce over
+//     __shfl_xor_sync (L-1 exchanges per lane per block) -- the paper's
+//     butterfly exchange, widened by the vector loads; it leaves every lane
+//     holding the block total of ONE row (its "own" token);
+//   * only the running block sums S_b are kept (shared memory, [b][lane]);
+//     the full K-entry table the reference stores (kernels.py:198-224) is
+//     never written: after the block bisection the selected block is
+//     re-read (L1/L2 hit) and its tree rebuilt in registers for the walk,
+//     which performs the same IEEE operations as the reference's
+//     cross-lane fetch walk.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "wd_device.cuh"
+
+namespace wd {
+
+enum { MODE_LDA = 0, MODE_ROWS = 1 };
+
+template <typename T> struct DrawParams {
+  const T* theta;  // LDA: doc rows (ld_theta); ROWS: unused
+  int64_t ld_theta;
+  const T* phi;  // LDA: word rows; ROWS: weight rows (ld_phi, 0 = shared)
+  int64_t ld_phi;
+  int32_t K;
+  const int64_t* offsets;   // LDA CSR offsets [n_docs + 1]
+  const int32_t* words;     // LDA [n_tokens]
+  const int32_t* token_doc; // LDA [n_tokens]
+  const int32_t* last_key;  // LDA master rule [n_docs]
+  int64_t n_tokens;         // LDA tokens / ROWS rows
+  int64_t doc_base;         // LDA global doc id of local doc 0 / ROWS row_base
+  int stop_mode;
+  int key_rule;
+  int lanes;  // reference W (prefix kernel: r and master groups only)
+  uint64_t seed;
+  const double* units;
+  const T* stops;
+  int32_t* z;
+  int32_t* word_topic;
+  int32_t* doc_topic;
+  unsigned long long* err;  // [0] AllZero key (min), [1] stop range flag
+};
+
+// Identity of the token/row a lane owns: global doc id (or row id), its hash
+// keys, and the error ordering key.
+template <typename T, int MODE>
+__device__ __forceinline__ void token_keys(const DrawParams<T>& p, int64_t tok, int32_t doc, int W,
+                                           uint64_t& ka, uint64_t& kb, unsigned long long& ekey,
+                                           int& r) {
+  if (MODE == MODE_ROWS) {
+    int64_t id = p.doc_base + tok;
+    ka = (uint64_t)id;
+    kb = 0;
+    ekey = (unsigned long long)id;
+    r = (int)(((id % W) + W) % W);
+  } else {
+    int64_t gm = p.doc_base + doc;
+    int64_t o0 = p.offsets[doc];
+    int64_t i = tok - o0;
+    int64_t key = i;
+    if (p.key_rule == WD_KEYS_MASTER) {
+      int64_t n = p.offsets[doc + 1] - o0;
+      if (i == n - 1 && p.stop_mode == WD_STOPS_SEEDED) key = p.last_key[doc];
+      ekey = ((unsigned long long)(gm / W) << 40) | ((unsigned long long)i << 8) |
+             (unsigned long long)(gm % W);
+    } else {
+      ekey = ((unsigned long long)gm << 32) | (unsigned long long)i;
+    }
+    ka = (uint64_t)gm;
+    kb = (uint64_t)key;
+    r = (int)(gm % W);
+  }
+}
+
+// kernels.py:95-101 (stop = fl(total * fl(u)), kept strictly below total)
+// plus the StopOutOfRangeError check of kernels.py:329-331 for explicit stops.
+template <typename T>
+__device__ __forceinline__ T make_stop(const DrawParams<T>& p, int64_t tok, T total, uint64_t ka,
+                                       uint64_t kb, bool rows) {
+  T stop;
+  if (p.stop_mode == WD_STOPS_EXPLICIT) {
+    stop = p.stops[tok];
+    bool live = total > T(0);
+    if (stop < T(0) || (live && stop >= total) || (!live && stop > T(0))) atomicOr(p.err + 1, 1ull);
+    return stop;
+  }
+  T uf;
+  if (p.stop_mode == WD_STOPS_UNITS) {
+    uf = from_double<T>(p.units[tok]);
+  } else if (p.stop_mode == WD_STOPS_PHILOX) {
+    uf = unit_to<T>(philox_bits(p.seed, ka, kb));
+  } else {
+    uf = unit_to<T>(rows ? unit_bits1(p.seed, ka) : unit_bits2(p.seed, ka, kb));
+  }
+  stop = mul_rn(total, uf);
+  if (!(total > T(0))) return T(0);
+  if (stop >= total) stop = next_below(total);
+  return stop;
+}
+
+// ============================================================== butterfly
+template <typename T, int W, bool VEC, int MODE, bool UNI>
+__device__ __forceinline__ T bfly_blocks(const DrawParams<T>& p, const T* const (&prow)[Geo<W>::L],
+                                         const T* const (&trow)[Geo<W>::L],
+                                         const bool (&rvalid)[Geo<W>::L], int nb, int rem, int s,
+                                         T acc, T* __restrict__ S, int lane) {
+  using G = Geo<W>;
+  constexpr int E = G::E, L = G::L;
+  for (int b = 0; b < nb; ++b) {
+    const int64_t off = (int64_t)rem + (int64_t)b * W;
+    T q[L];
+    Seg<T, E, VEC> th_u;
+    if (MODE == MODE_LDA && UNI) th_u.load(trow[0] + off);
+#pragma unroll
+    for (int kk = 0; kk < L; ++kk) {
+      Seg<T, E, VEC> x;
+      if (rvalid[kk]) x.load(prow[kk] + off); else x.zero();
+      T a[E];
+      if (MODE == MODE_LDA) {
+        Seg<T, E, VEC> th;
+        if (UNI) th = th_u;
+        else if (rvalid[kk]) th.load(trow[kk] + off);
+        else th.zero();
+#pragma unroll
+        for (int e = 0; e < E; ++e) a[e] = mul_rn(th.v[e], x.v[e]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) a[e] = x.v[e];
+      }
+      q[kk] = Tree<T, E>::sum(a);  // first log2(E) butterfly levels, in registers
+    }
+    // remaining log2(L) levels: transpose-reduce over lanes s ^ bit
+#pragma unroll
+    for (int bit = 1, n = L; bit < L; bit <<= 1, n >>= 1) {
+      const bool hi = (s & bit) != 0;
+#pragma unroll
+      for (int t = 0; t < n / 2; ++t) {
+        T x0 = q[2 * t], x1 = q[2 * t + 1];
+        T send = hi ? x0 : x1;
+        T keep = hi ? x1 : x0;
+        q[t] = add_rn(keep, __shfl_xor_sync(FULL, send, bit));
+      }
+    }
+    acc = add_rn(acc, q[0]);  // sequential accumulation over blocks (kernels.py:221-223)
+    S[b * 32 + lane] = acc;
+  }
+  return acc;
+}
+
+// In-block walk (kernels.py:268-314).  Per level the reference compares stop
+// with low + node(lo, lo+bit-1) or with high - node(lo+bit, lo+2bit-1), picked
+// by bit `bit` of r = doc mod W; the nodes are the block's pairwise-tree nodes
+// (what its cross-lane fetch of the butterfly table returns).  cur[0, 2*BIT)
+// holds the products of the live range; the range halves every level.
+template <typename T, int BIT> struct Walk {
+  static __device__ __forceinline__ void run(T* cur, T& low, T& high, T stop, int r, int& lo) {
+    const T cmp = (r & BIT) ? sub_rn(high, Tree<T, BIT>::sum(cur + BIT)) : add_rn(low, Tree<T, BIT>::sum(cur));
+    const bool less = stop < cmp;
+    if (less) high = cmp;
+    else { low = cmp; lo += BIT; }
+#pragma unroll
+    for (int t = 0; t < BIT; ++t) cur[t] = less ? cur[t] : cur[t + BIT];
+    Walk<T, BIT / 2>::run(cur, low, high, stop, r, lo);
+  }
+};
+template <typename T> struct Walk<T, 0> {
+  static __device__ __forceinline__ void run(T*, T&, T&, T, int, int&) {}
+};
+
+template <typename T, int W, bool VEC, int MODE>
+__global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
+  using G = Geo<W>;
+  constexpr int E = G::E, L = G::L, R = G::R;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int K = p.K;
+  const int nb = K / W, rem = K % W;
+  T* S = reinterpret_cast<T*>(smem_raw) + (size_t)wib * (size_t)(nb > 0 ? nb : 1) * 32;
+  const int s = lane % L;
+  const int rg = lane / L;
+  const int own = s * R + rg;  // chunk row this lane ends up owning
+  const int64_t n = p.n_tokens;
+  const int64_t n_chunks = (n + 31) >> 5;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t c = (int64_t)blockIdx.x * wpb + wib; c < n_chunks; c += (int64_t)gridDim.x * wpb) {
+    const int64_t tok0 = c << 5;
+    const bool my_valid = tok0 + lane < n;
+    int32_t my_doc = 0, my_word = 0;
+    if (MODE == MODE_LDA && my_valid) {
+      my_doc = p.token_doc[tok0 + lane];
+      my_word = p.words[tok0 + lane];
+    }
+    const T* prow[L];
+    const T* trow[L];
+    bool rvalid[L];
+#pragma unroll
+    for (int kk = 0; kk < L; ++kk) {
+      const int k = kk * R + rg;
+      rvalid[kk] = tok0 + k < n;
+      if (MODE == MODE_LDA) {
+        const int32_t wk = __shfl_sync(FULL, my_word, k);
+        const int32_t dk = __shfl_sync(FULL, my_doc, k);
+        prow[kk] = p.phi + (int64_t)wk * p.ld_phi + s * E;
+        trow[kk] = p.theta + (int64_t)dk * p.ld_theta + s * E;
+      } else {
+        prow[kk] = p.phi + (tok0 + k) * p.ld_phi + s * E;
+        trow[kk] = nullptr;
+      }
+    }
+    const int64_t own_tok = tok0 + own;
+    const bool own_valid = own_tok < n;
+    const int32_t own_doc = __shfl_sync(FULL, my_doc, own);
+    const int32_t own_word = __shfl_sync(FULL, my_word, own);
+    const T* pown = p.phi + (MODE == MODE_LDA ? (int64_t)own_word : own_tok) * p.ld_phi;
+    const T* town = MODE == MODE_LDA ? p.theta + (int64_t)own_doc * p.ld_theta : nullptr;
+
+    // remnant: sequential running sums of the own row (kernels.py:199-205)
+    T acc = T(0);
+    if (own_valid) {
+      for (int t = 0; t < rem; ++t) {
+        T a = MODE == MODE_LDA ? mul_rn(__ldg(town + t), __ldg(pown + t)) : __ldg(pown + t);
+        acc = add_rn(acc, a);
+      }
+    }
+    const T prem = acc;
+    bool uni = false;
+    if (MODE == MODE_LDA) {
+      const int32_t d0 = __shfl_sync(FULL, my_doc, 0);
+      uni = __all_sync(FULL, !my_valid || my_doc == d0);
+    }
+    if (uni) acc = bfly_blocks<T, W, VEC, MODE, true>(p, prow, trow, rvalid, nb, rem, s, acc, S, lane);
+    else acc = bfly_blocks<T, W, VEC, MODE, false>(p, prow, trow, rvalid, nb, rem, s, acc, S, lane);
+    __syncwarp();
+    const T total = acc;
+
+    if (own_valid) {
+      uint64_t ka, kb;
+      unsigned long long ekey;
+      int r;
+      token_keys<T, MODE>(p, own_tok, own_doc, W, ka, kb, ekey, r);
+      const T stop = make_stop<T>(p, own_tok, total, ka, kb, MODE == MODE_ROWS);
+      if (!(total > T(0))) atomicMin(p.err, ekey);
+      // block bisection over S (kernels.py:337-346)
+      int j = 0, k = nb - 1;
+      while (j < k) {
+        const int mid = (j + k) >> 1;
+        if (stop < S[mid * 32 + lane]) k = mid; else j = mid + 1;
+      }
+      const int64_t bb = (int64_t)rem + (int64_t)j * W;
+      const T prev = bb > 0 ? (j > 0 ? S[(j - 1) * 32 + lane] : prem) : T(0);
+      const bool fallback = bb > 0 && stop < prev && total > T(0);
+      int result = 0;
+      if (nb > 0 && !fallback) {
+        // rebuild the selected block's products (own row) and walk it
+        T cur[W];
+#pragma unroll
+        for (int g = 0; g < W / E; ++g) {
+          Seg<T, E, VEC> x;
+          x.load(pown + bb + g * E);
+          if (MODE == MODE_LDA) {
+            Seg<T, E, VEC> th;
+            th.load(town + bb + g * E);
+#pragma unroll
+            for (int e = 0; e < E; ++e) cur[g * E + e] = mul_rn(th.v[e], x.v[e]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) cur[g * E + e] = x.v[e];
+          }
+        }
+        T low = prev, high = S[j * 32 + lane];
+        int lo = 0;
+        Walk<T, W / 2>::run(cur, low, high, stop, r, lo);
+        result = (int)bb + lo;
+      }
+      if (fallback) {
+        // linear remnant fallback (kernels.py:354-361)
+        T a2 = T(0);
+        for (int t = 0; t < rem; ++t) {
+          T a = MODE == MODE_LDA ? mul_rn(__ldg(town + t), __ldg(pown + t)) : __ldg(pown + t);
+          a2 = add_rn(a2, a);
+          if (stop < a2) { result = t; break; }
+        }
+      }
+      p.z[own_tok] = result;
+      if (MODE == MODE_LDA) {
+        if (p.word_topic) atomicAdd(p.word_topic + (int64_t)own_word * K + result, 1);
+        if (p.doc_topic) atomicAdd(p.doc_topic + (int64_t)own_doc * K + result, 1);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ========================================================= prefix table
+// The paper's comparison baseline: a full per-token prefix-sum table
+// (kernels.py:129-167 compute_partial_sums_transposed + kernels.py:248-260
+// _prefix_binary_search; arithmetic identical to draw_z_basic,
+// kernels.py:380-401).  Loads are the same coalesced vector loads as the
+// butterfly kernel; the products are transposed back to their row through a
+// padded shared-memory tile (the "pay the piper" gather),
+// summed sequentially, and EVERY running sum is stored to a per-lane table in
+// global scratch (the paper's local-memory table, interleaved by lane so the
+// stores coalesce).  The bisection then reads that table.
+template <typename T, bool VEC, int MODE>
+__global__ void __launch_bounds__(128) prefix_kernel(DrawParams<T> p, T* __restrict__ table,
+                                                     int64_t stride) {
+  constexpr int W = 32;
+  using G = Geo<W>;
+  constexpr int E = G::E, L = G::L, R = G::R;
+  constexpr int TP = W + 1;  // padded tile row
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  T* tile = reinterpret_cast<T*>(smem_raw) + (size_t)wib * 32 * TP;
+  const int K = p.K;
+  const int nb = K / W, rem = K % W;
+  const int s = lane % L;
+  const int rg = lane / L;
+  const int64_t gl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // table column
+  const int64_t n = p.n_tokens;
+  const int64_t n_chunks = (n + 31) >> 5;
+  const int64_t wpb = blockDim.x >> 5;
+  const int WR = p.lanes;
+  for (int64_t c = (int64_t)blockIdx.x * wpb + wib; c < n_chunks; c += (int64_t)gridDim.x * wpb) {
+    const int64_t tok0 = c << 5;
+    const bool my_valid = tok0 + lane < n;
+    int32_t my_doc = 0, my_word = 0;
+    if (MODE == MODE_LDA && my_valid) {
+      my_doc = p.token_doc[tok0 + lane];
+      my_word = p.words[tok0 + lane];
+    }
+    const T* pown = p.phi + (MODE == MODE_LDA ? (int64_t)my_word : tok0 + lane) * p.ld_phi;
+    const T* town = MODE == MODE_LDA ? p.theta + (int64_t)my_doc * p.ld_theta : nullptr;
+    T acc = T(0);
+    if (my_valid) {
+      for (int t = 0; t < rem; ++t) {
+        T a = MODE == MODE_LDA ? mul_rn(__ldg(town + t), __ldg(pown + t)) : __ldg(pown + t);
+        acc = add_rn(acc, a);
+        table[(int64_t)t * stride + gl] = acc;
+      }
+    }
+    for (int b = 0; b < nb; ++b) {
+      const int64_t off = (int64_t)rem + (int64_t)b * W;
+#pragma unroll
+      for (int kk = 0; kk < L; ++kk) {
+        const int k = kk * R + rg;
+        const int32_t wk = __shfl_sync(FULL, my_word, k);
+        const int32_t dk = __shfl_sync(FULL, my_doc, k);
+        Seg<T, E, VEC> x;
+        const bool v = tok0 + k < n;
+        if (v) x.load(p.phi + (MODE == MODE_LDA ? (int64_t)wk : tok0 + k) * p.ld_phi + off + s * E);
+        else x.zero();
+        if (MODE == MODE_LDA) {
+          Seg<T, E, VEC> th;
+          if (v) th.load(p.theta + (int64_t)dk * p.ld_theta + off + s * E); else th.zero();
+#pragma unroll
+          for (int e = 0; e < E; ++e) x.v[e] = mul_rn(th.v[e], x.v[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) tile[k * TP + s * E + e] = x.v[e];
+      }
+      __syncwarp();
+#pragma unroll 8
+      for (int t = 0; t < W; ++t) {
+        acc = add_rn(acc, tile[lane * TP + t]);
+        table[(off + t) * stride + gl] = acc;
+      }
+      __syncwarp();
+    }
+    const T total = acc;
+    if (my_valid) {
+      uint64_t ka, kb;
+      unsigned long long ekey;
+      int r;
+      token_keys<T, MODE>(p, tok0 + lane, my_doc, WR, ka, kb, ekey, r);
+      const T stop = make_stop<T>(p, tok0 + lane, total, ka, kb, MODE == MODE_ROWS);
+      if (!(total > T(0))) atomicMin(p.err, ekey);
+      int j = 0, k = K - 1;  // samp.py:65-77 bisection over the table
+      while (j < k) {
+        const int mid = (j + k) >> 1;
+        if (stop < table[(int64_t)mid * stride + gl]) k = mid; else j = mid + 1;
+      }
+      p.z[tok0 + lane] = j;
+      if (MODE == MODE_LDA) {
+        if (p.word_topic) atomicAdd(p.word_topic + (int64_t)my_word * K + j, 1);
+        if (p.doc_topic) atomicAdd(p.doc_topic + (int64_t)my_doc * K + j, 1);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace wd

@@ -1,0 +1,6 @@
+// Explicit instantiation of the draw kernels for float (see wd_launch.cuh).
+#include "wd_launch.cuh"
+
+namespace wd {
+template int launch_draw<float>(int, int, bool, int, const DrawParams<float>&, void*, size_t, cudaStream_t);
+}  // namespace wd

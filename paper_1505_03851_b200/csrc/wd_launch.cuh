@@ -1,0 +1,121 @@
+// wd_launch.cuh -- host-side instantiation and launch of the draw kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
+
+#include "wd_draw.cuh"
+
+namespace wd {
+
+constexpr int kThreads = 128;          // 4 warps per CTA
+constexpr int kPrefixBlocksPerSM = 8;  // persistent grid of the prefix baseline
+
+int device_sm_count();
+void set_last_cuda_error(cudaError_t e);
+
+inline int occupancy_blocks(const void* fn, size_t smem, int threads = kThreads) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, size_t>, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(fn, smem * 1024 + (size_t)threads);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int nb = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem);
+  if (e != cudaSuccess) {
+    set_last_cuda_error(e);
+    nb = 0;
+  }
+  cache[key] = nb;
+  return nb;
+}
+
+// shared memory of one warp's running block sums S[b][lane]
+template <typename T>
+inline size_t bfly_smem_per_warp(int W, int K) {
+  int nb = K / W;
+  return (size_t)(nb > 0 ? nb : 1) * 32 * sizeof(T);
+}
+template <typename T>
+inline size_t prefix_smem() {
+  return (size_t)(kThreads / 32) * 32 * 33 * sizeof(T);
+}
+inline int64_t prefix_table_cols() { return (int64_t)device_sm_count() * kPrefixBlocksPerSM * kThreads; }
+
+template <typename T, int W, bool VEC, int MODE>
+int launch_bfly_inst(const DrawParams<T>& p, cudaStream_t st) {
+  const void* fn = (const void*)bfly_kernel<T, W, VEC, MODE>;
+  const size_t per_warp = bfly_smem_per_warp<T>(W, p.K);
+  int wpb = kThreads / 32;  // fewer warps per CTA when the block sums are large
+  while (wpb > 1 && (size_t)wpb * per_warp > 227 * 1024) wpb >>= 1;
+  const size_t smem = (size_t)wpb * per_warp;
+  if (smem > 227 * 1024) return WD_ERR_UNSUPPORTED;
+  const int threads = wpb * 32;
+  int per_sm = occupancy_blocks(fn, smem, threads);
+  if (per_sm <= 0) return WD_ERR_CUDA;
+  int64_t chunks = (p.n_tokens + 31) / 32;
+  int64_t want = (chunks + wpb - 1) / wpb;
+  int64_t cap = (int64_t)per_sm * device_sm_count();
+  int grid = (int)(want < cap ? want : cap);
+  if (grid <= 0) return WD_OK;
+  bfly_kernel<T, W, VEC, MODE><<<grid, threads, smem, st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { set_last_cuda_error(e); return WD_ERR_CUDA; }
+  return WD_OK;
+}
+
+template <typename T, bool VEC, int MODE>
+int launch_prefix_inst(const DrawParams<T>& p, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const void* fn = (const void*)prefix_kernel<T, VEC, MODE>;
+  size_t smem = prefix_smem<T>();
+  int64_t cols = prefix_table_cols();
+  size_t need = (size_t)cols * (size_t)p.K * sizeof(T);
+  if (ws == nullptr || ws_bytes < need) return WD_ERR_WORKSPACE;
+  if (occupancy_blocks(fn, smem) <= 0) return WD_ERR_CUDA;
+  int grid = (int)(cols / kThreads);
+  prefix_kernel<T, VEC, MODE><<<grid, kThreads, smem, st>>>(p, reinterpret_cast<T*>(ws), cols);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { set_last_cuda_error(e); return WD_ERR_CUDA; }
+  return WD_OK;
+}
+
+template <typename T, bool VEC, int MODE>
+int launch_bfly_w(int W, const DrawParams<T>& p, cudaStream_t st) {
+  switch (W) {
+    case 2: return launch_bfly_inst<T, 2, VEC, MODE>(p, st);
+    case 4: return launch_bfly_inst<T, 4, VEC, MODE>(p, st);
+    case 8: return launch_bfly_inst<T, 8, VEC, MODE>(p, st);
+    case 16: return launch_bfly_inst<T, 16, VEC, MODE>(p, st);
+    case 32: return launch_bfly_inst<T, 32, VEC, MODE>(p, st);
+    case 64: return launch_bfly_inst<T, 64, VEC, MODE>(p, st);
+    default: return WD_ERR_UNSUPPORTED;
+  }
+}
+
+// Dispatch on (variant, W, VEC, MODE); explicit instantiations live in
+// wd_draw_f32.cu / wd_draw_f64.cu so the two element types compile in parallel.
+template <typename T>
+int launch_draw(int variant, int W, bool vec, int mode, const DrawParams<T>& p, void* ws,
+                size_t ws_bytes, cudaStream_t st) {
+  if (variant == WD_BUTTERFLY) {
+    if (mode == MODE_LDA)
+      return vec ? launch_bfly_w<T, true, MODE_LDA>(W, p, st) : launch_bfly_w<T, false, MODE_LDA>(W, p, st);
+    return vec ? launch_bfly_w<T, true, MODE_ROWS>(W, p, st) : launch_bfly_w<T, false, MODE_ROWS>(W, p, st);
+  }
+  if (variant == WD_PREFIX) {
+    if (mode == MODE_LDA)
+      return vec ? launch_prefix_inst<T, true, MODE_LDA>(p, ws, ws_bytes, st)
+                 : launch_prefix_inst<T, false, MODE_LDA>(p, ws, ws_bytes, st);
+    return vec ? launch_prefix_inst<T, true, MODE_ROWS>(p, ws, ws_bytes, st)
+               : launch_prefix_inst<T, false, MODE_ROWS>(p, ws, ws_bytes, st);
+  }
+  return WD_ERR_INVALID_ARGUMENT;
+}
+
+}  // namespace wd

@@ -1,0 +1,348 @@
+// wd_resample.cu -- throughput-mode Dirichlet resample and log-likelihood on
+// the device.
+//
+// Reference: lda.py:185-208 resample_params
+//     theta[m]   ~ Dir(alpha + doc_topic[m])   (row-normalised Gammas)
+//     phi[:, k]  ~ Dir(beta  + word_topic[:, k]) (column-normalised Gammas)
+// and lda.py:289-305 log_likelihood.
+//
+// Statistical (not bitwise) parity: the reference draws its Gammas from
+// numpy's PCG64 stream, which has no device equivalent.  Here every Gamma
+// is drawn from a counter-based Philox4x32-10 stream keyed by
+// (seed, row, topic) -- so the result is independent of launch geometry and
+// of the number of GPUs -- with Marsaglia-Tsang (shape < 1 boosted by
+// U^(1/a)) evaluated in LOG space, so the tiny Gammas of alpha = 0.1 /
+// beta = 0.01 shapes never underflow before normalisation.  Reductions use a
+// fixed order, so a given (seed, counts) always gives the same bits.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "warpdraw_b200.h"
+#include "wd_device.cuh"
+
+namespace wd {
+
+int device_sm_count();
+void set_last_cuda_error(cudaError_t e);
+
+struct Philox4 {
+  uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ Philox4 philox4(uint64_t seed, uint64_t row, uint32_t k, uint32_t ctr) {
+  uint32_t c0 = (uint32_t)row, c1 = (uint32_t)(row >> 32), c2 = k, c3 = ctr;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  return {c0, c1, c2, c3};
+}
+
+// uniform in (0, 1): 24-bit mantissa, never 0
+__device__ __forceinline__ float u01(uint32_t x) { return ((float)(x >> 8) + 0.5f) * 0x1p-24f; }
+
+// log of a Gamma(a, 1) variate (Marsaglia & Tsang 2000; a < 1 via the
+// boost Gamma(a) = Gamma(a + 1) * U^(1/a), the same construction numpy uses).
+__device__ float log_gamma_draw(float a, uint64_t seed, uint64_t row, uint32_t k) {
+  uint32_t ctr = 0;
+  Philox4 r = philox4(seed, row, k, ctr++);
+  float boost = 0.f;
+  if (a < 1.f) {
+    boost = logf(u01(r.w)) / a;
+    a += 1.f;
+  }
+  const float d = a - (1.f / 3.f);
+  const float c = rsqrtf(9.f * d);
+  for (int attempt = 0; attempt < 64; ++attempt) {
+    if (attempt > 0) r = philox4(seed, row, k, ctr++);
+    // Box-Muller normal from (x, y)
+    const float rad = sqrtf(-2.f * logf(u01(r.x)));
+    float s, co;
+    sincospif(2.f * u01(r.y), &s, &co);
+    const float x = rad * co;
+    float v = 1.f + c * x;
+    if (v <= 0.f) continue;
+    v = v * v * v;
+    const float u = u01(r.z);
+    const float x2 = x * x;
+    if (u < 1.f - 0.0331f * x2 * x2 || logf(u) < 0.5f * x2 + d * (1.f - v + logf(v)))
+      return logf(d) + logf(v) + boost;
+  }
+  return logf(d) + boost;  // unreachable in practice (acceptance > 95% per attempt)
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// theta[m, :] ~ Dir(alpha + hist(z of doc m)); one warp per document; the
+// doc-topic histogram never touches HBM (it lives in the warp's smem slice).
+template <typename T>
+__global__ void __launch_bounds__(256) theta_kernel(const int32_t* __restrict__ z, const int64_t* __restrict__ off,
+                                                    int64_t n_docs, int32_t K, float alpha, uint64_t seed,
+                                                    int64_t doc_base, T* __restrict__ theta, int64_t ld) {
+  extern __shared__ float tsm[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  float* lg = tsm + (size_t)wib * K;
+  int* hist = reinterpret_cast<int*>(lg);
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t m = (int64_t)blockIdx.x * wpb + wib; m < n_docs; m += (int64_t)gridDim.x * wpb) {
+    for (int k = lane; k < K; k += 32) hist[k] = 0;
+    __syncwarp();
+    const int64_t a = off[m], b = off[m + 1];
+    for (int64_t t = a + lane; t < b; t += 32) atomicAdd(hist + z[t], 1);
+    __syncwarp();
+    const uint64_t row = (uint64_t)(doc_base + m);
+    float mx = -INFINITY;
+    for (int k = lane; k < K; k += 32) {
+      const float v = log_gamma_draw(alpha + (float)hist[k], seed, row, (uint32_t)k);
+      lg[k] = v;
+      mx = fmaxf(mx, v);
+    }
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int k = lane; k < K; k += 32) {
+      const float e = expf(lg[k] - mx);
+      lg[k] = e;
+      sum += e;
+    }
+    sum = warp_sum(sum);
+    const float inv = 1.f / sum;
+    T* out = theta + m * ld;
+    for (int k = lane; k < K; k += 32) out[k] = (T)(lg[k] * inv);
+    __syncwarp();
+  }
+}
+
+// phi[:, k] ~ Dir(beta + word_topic[:, k]): three passes over V x K with
+// per-CTA column partials reduced in a fixed order (deterministic).
+constexpr int kPhiThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kPhiThreads) phi_pass(int pass, const int32_t* __restrict__ wt, int64_t V,
+                                                        int32_t K, float beta, uint64_t seed, T* __restrict__ phi,
+                                                        int64_t ld, float* __restrict__ part,
+                                                        const float* __restrict__ colstat) {
+  const int64_t rows_per = (V + gridDim.x - 1) / gridDim.x;
+  const int64_t v0 = (int64_t)blockIdx.x * rows_per;
+  const int64_t v1 = v0 + rows_per < V ? v0 + rows_per : V;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    float acc = pass == 0 ? -INFINITY : 0.f;
+    const float cs = pass == 0 ? 0.f : colstat[k];
+    for (int64_t v = v0; v < v1; ++v) {
+      T* p = phi + v * ld + k;
+      if (pass == 0) {
+        const float lgv = log_gamma_draw(beta + (float)wt[v * (int64_t)K + k], seed, (uint64_t)v, (uint32_t)k);
+        *p = (T)lgv;
+        acc = fmaxf(acc, lgv);
+      } else if (pass == 1) {
+        const float e = expf((float)*p - cs);
+        *p = (T)e;
+        acc += e;
+      } else {
+        *p = (T)((float)*p / cs);
+      }
+    }
+    if (pass < 2) part[(int64_t)blockIdx.x * K + k] = acc;
+  }
+}
+
+__global__ void col_reduce(int pass, const float* __restrict__ part, int G, int32_t K, float* __restrict__ colstat) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  float acc = pass == 0 ? -INFINITY : 0.f;
+  for (int g = 0; g < G; ++g) {
+    const float v = part[(int64_t)g * K + k];
+    acc = pass == 0 ? fmaxf(acc, v) : acc + v;
+  }
+  colstat[k] = acc;
+}
+
+// log-likelihood: sum over tokens of log(theta_hat[m] . phi_hat[w]) where
+// theta_hat = theta / rowsum, phi_hat = phi / colsum (lda.py:289-305).
+// One warp per 32-token chunk; per token a K-dot over coalesced rows.
+template <typename T>
+__global__ void __launch_bounds__(256) ll_kernel(const T* __restrict__ theta, int64_t ldt, const T* __restrict__ phi,
+                                                 int64_t ldp, const int32_t* __restrict__ words,
+                                                 const int32_t* __restrict__ td, int64_t n, int32_t K,
+                                                 const double* __restrict__ inv_rows,
+                                                 const double* __restrict__ inv_cols, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double acc = 0.0;
+  for (int64_t t = gw; t < n; t += nw) {
+    const int32_t m = td[t], w = words[t];
+    const T* th = theta + (int64_t)m * ldt;
+    const T* ph = phi + (int64_t)w * ldp;
+    double dot = 0.0;
+    for (int k = lane; k < K; k += 32) dot += (double)th[k] * (double)ph[k] * inv_cols[k];
+    dot = warp_sum_d(dot) * inv_rows[m];
+    if (lane == 0) acc += log(dot);
+  }
+  if (lane == 0) atomicAdd(out, acc);
+}
+
+template <typename T>
+__global__ void row_inv_sums(const T* __restrict__ theta, int64_t ld, int64_t n_docs, int32_t K, double* __restrict__ inv) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t m = gw; m < n_docs; m += nw) {
+    double s = 0.0;
+    for (int k = lane; k < K; k += 32) s += (double)theta[m * ld + k];
+    s = warp_sum_d(s);
+    if (lane == 0) inv[m] = 1.0 / s;
+  }
+}
+
+template <typename T>
+__global__ void col_inv_sums(const T* __restrict__ phi, int64_t ld, int64_t V, int32_t K, double* __restrict__ inv) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double s = 0.0;
+  for (int64_t v = 0; v < V; ++v) s += (double)phi[v * ld + k];
+  inv[k] = 1.0 / s;
+}
+
+static int ck() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_last_cuda_error(e);
+    return WD_ERR_CUDA;
+  }
+  return WD_OK;
+}
+
+static int phi_grid() { return device_sm_count() * 4; }
+
+template <typename T>
+static int resample_theta_t(const int32_t* z, const int64_t* off, int64_t n_docs, int32_t K, float alpha, uint64_t seed,
+                            int64_t doc_base, T* theta, int64_t ld, cudaStream_t st) {
+  const int threads = 256;
+  size_t smem = (size_t)(threads / 32) * K * sizeof(float);
+  int wpb = threads / 32;
+  int th = threads;
+  while (smem > 200 * 1024 && wpb > 1) {
+    wpb /= 2;
+    th = wpb * 32;
+    smem = (size_t)wpb * K * sizeof(float);
+  }
+  if (smem > 227 * 1024) return WD_ERR_UNSUPPORTED;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute((const void*)theta_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int64_t want = (n_docs + wpb - 1) / wpb;
+  int64_t cap = (int64_t)device_sm_count() * 64;
+  int grid = (int)(want < cap ? want : cap);
+  if (grid < 1) return WD_OK;
+  theta_kernel<T><<<grid, th, smem, st>>>(z, off, n_docs, K, alpha, seed, doc_base, theta, ld);
+  return ck();
+}
+
+template <typename T>
+static int resample_phi_t(const int32_t* wt, int64_t V, int32_t K, float beta, uint64_t seed, T* phi, int64_t ld,
+                          void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int G = phi_grid();
+  size_t need = ((size_t)G * K + 2 * (size_t)K) * sizeof(float);
+  if (!ws || ws_bytes < need) return WD_ERR_WORKSPACE;
+  float* part = (float*)ws;
+  float* colstat = part + (size_t)G * K;
+  int cb = (K + 255) / 256;
+  phi_pass<T><<<G, kPhiThreads, 0, st>>>(0, wt, V, K, beta, seed, phi, ld, part, nullptr);
+  col_reduce<<<cb, 256, 0, st>>>(0, part, G, K, colstat);
+  phi_pass<T><<<G, kPhiThreads, 0, st>>>(1, wt, V, K, beta, seed, phi, ld, part, colstat);
+  col_reduce<<<cb, 256, 0, st>>>(1, part, G, K, colstat + K);
+  phi_pass<T><<<G, kPhiThreads, 0, st>>>(2, wt, V, K, beta, seed, phi, ld, part, colstat + K);
+  return ck();
+}
+
+template <typename T>
+static int ll_t(const T* theta, int64_t ldt, const T* phi, int64_t ldp, const int32_t* words, const int32_t* td,
+                int64_t n_docs, int64_t n_tokens, int64_t V, int32_t K, double* out, void* ws, size_t ws_bytes,
+                cudaStream_t st) {
+  size_t need = ((size_t)n_docs + (size_t)K) * sizeof(double);
+  if (!ws || ws_bytes < need) return WD_ERR_WORKSPACE;
+  double* inv_rows = (double*)ws;
+  double* inv_cols = inv_rows + n_docs;
+  cudaMemsetAsync(out, 0, sizeof(double), st);
+  int g = device_sm_count() * 8;
+  if (n_docs > 0) row_inv_sums<T><<<g, 256, 0, st>>>(theta, ldt, n_docs, K, inv_rows);
+  col_inv_sums<T><<<(K + 127) / 128, 128, 0, st>>>(phi, ldp, V, K, inv_cols);
+  if (n_tokens > 0) ll_kernel<T><<<g, 256, 0, st>>>(theta, ldt, phi, ldp, words, td, n_tokens, K, inv_rows, inv_cols, out);
+  return ck();
+}
+
+}  // namespace wd
+
+using namespace wd;
+
+extern "C" {
+
+int wd_resample_theta(int dtype, const int32_t* z, const int64_t* doc_offsets, int64_t n_docs, int32_t n_topics,
+                      double alpha, uint64_t seed, int64_t doc_base, void* theta, int64_t ld_theta, void* stream) {
+  if (n_docs < 0 || n_topics <= 0 || !doc_offsets || !theta || ld_theta < n_topics || alpha <= 0)
+    return WD_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == WD_FLOAT32)
+    return resample_theta_t<float>(z, doc_offsets, n_docs, n_topics, (float)alpha, seed, doc_base, (float*)theta,
+                                   ld_theta, st);
+  if (dtype == WD_FLOAT64)
+    return resample_theta_t<double>(z, doc_offsets, n_docs, n_topics, (float)alpha, seed, doc_base, (double*)theta,
+                                    ld_theta, st);
+  return WD_ERR_INVALID_ARGUMENT;
+}
+
+size_t wd_resample_phi_workspace_bytes(int32_t n_topics) {
+  return ((size_t)phi_grid() * n_topics + 2 * (size_t)n_topics) * sizeof(float);
+}
+
+int wd_resample_phi(int dtype, const int32_t* word_topic, int64_t vocab_size, int32_t n_topics, double beta,
+                    uint64_t seed, void* phi, int64_t ld_phi, void* workspace, size_t workspace_bytes, void* stream) {
+  if (vocab_size <= 0 || n_topics <= 0 || !word_topic || !phi || ld_phi < n_topics || beta <= 0)
+    return WD_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == WD_FLOAT32)
+    return resample_phi_t<float>(word_topic, vocab_size, n_topics, (float)beta, seed, (float*)phi, ld_phi, workspace,
+                                 workspace_bytes, st);
+  if (dtype == WD_FLOAT64)
+    return resample_phi_t<double>(word_topic, vocab_size, n_topics, (float)beta, seed, (double*)phi, ld_phi,
+                                  workspace, workspace_bytes, st);
+  return WD_ERR_INVALID_ARGUMENT;
+}
+
+int wd_log_likelihood(int dtype, const void* theta, int64_t ld_theta, const void* phi, int64_t ld_phi,
+                      const int32_t* words, const int32_t* token_doc, int64_t n_docs, int64_t n_tokens,
+                      int64_t vocab_size, int32_t n_topics, double* out, void* workspace, size_t workspace_bytes,
+                      void* stream) {
+  if (n_topics <= 0 || !theta || !phi || !out || n_docs < 0 || n_tokens < 0) return WD_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == WD_FLOAT32)
+    return ll_t<float>((const float*)theta, ld_theta, (const float*)phi, ld_phi, words, token_doc, n_docs, n_tokens,
+                       vocab_size, n_topics, out, workspace, workspace_bytes, st);
+  if (dtype == WD_FLOAT64)
+    return ll_t<double>((const double*)theta, ld_theta, (const double*)phi, ld_phi, words, token_doc, n_docs,
+                        n_tokens, vocab_size, n_topics, out, workspace, workspace_bytes, st);
+  return WD_ERR_INVALID_ARGUMENT;
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+"""Throughput-mode LDA: corpus, theta, phi, z and counts resident in HBM.
+
+One Gibbs iteration (lda.py:211-242 semantics, uncollapsed):
+
+    word_topic = 0
+    z ~ draw (butterfly kernel, SeededStops(derive_seed(seed, 1, t)))
+        with word_topic += 1 fused into the draw epilogue
+    all_reduce(word_topic, SUM)                      # NCCL, only if sharded
+    phi[:, k]  ~ Dir(beta + word_topic[:, k])        # wd_resample_phi
+    theta[m]   ~ Dir(alpha + hist(z of doc m))       # wd_resample_theta
+
+Documents are sharded across ranks in 32-aligned contiguous ranges; the
+global doc id drives both the u hash and the theta Gamma stream, and phi is
+resampled from the all-reduced counts with the same key on every rank, so a
+run is independent of the number of GPUs (tests/test_multigpu.py).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .kernels import DeviceCorpus, SeededStops, draw_z_device, raise_for_err
+from .rng import derive_seed
+
+
+class DeviceLDA:
+    def __init__(self, corpus: DeviceCorpus, n_topics: int, vocab_size: int, *, lanes: int = 32, dtype=None,
+                 alpha: float = 0.1, beta: float = 0.01, seed: int = 0, kernel: str = "butterfly",
+                 process_group=None, theta=None, phi=None):
+        import torch
+
+        _lib.require_cuda()
+        self.torch = torch
+        self.corpus = corpus
+        self.K = int(n_topics)
+        self.V = int(vocab_size)
+        self.lanes = int(lanes)
+        self.dtype = dtype or torch.float32
+        self.alpha, self.beta, self.seed = float(alpha), float(beta), int(seed)
+        self.kernel = kernel
+        self.pg = process_group
+        dev = corpus.offsets.device
+        self.device = dev
+        self.theta = theta if theta is not None else torch.empty((corpus.n_docs, self.K), dtype=self.dtype, device=dev)
+        self.phi = phi if phi is not None else torch.empty((self.V, self.K), dtype=self.dtype, device=dev)
+        self.z = torch.zeros(corpus.n_tokens, dtype=torch.int32, device=dev)
+        self.word_topic = torch.zeros((self.V, self.K), dtype=torch.int32, device=dev)
+        self.err = torch.empty(2, dtype=torch.int64, device=dev)
+        L = _lib.load()
+        self._phi_ws = torch.empty(int(L.wd_resample_phi_workspace_bytes(self.K)), dtype=torch.uint8, device=dev)
+        self._ll_ws = torch.empty(8 * (corpus.n_docs + self.K) + 8, dtype=torch.uint8, device=dev)
+        self._ll_out = torch.zeros(1, dtype=torch.float64, device=dev)
+        self._dt = _lib.WD_FLOAT32 if self.dtype == torch.float32 else _lib.WD_FLOAT64
+
+    # ------------------------------------------------------------ init
+    def init_uniform(self, low: float = 0.1, high: float = 1.0, seed: int | None = None):
+        """synth_params-style positive weights (bench.py:187-192 of the reference)."""
+        torch = self.torch
+        g = torch.Generator(device=self.device).manual_seed(int(self.seed if seed is None else seed))
+        self.theta.uniform_(low, high, generator=g)
+        self.phi.uniform_(low, high, generator=g)
+
+    def init_from_assignments(self, t: int = -1):
+        """init_assignments + resample at iteration -1 (lda.py:264-265), device RNG."""
+        torch = self.torch
+        g = torch.Generator(device=self.device).manual_seed(int(derive_seed(self.seed, 0, self.corpus.doc_base)))
+        self.z.random_(0, self.K, generator=g)
+        self.word_topic.zero_()
+        L = _lib.load()
+        _lib.check(L.wd_topic_counts(self.corpus.words.data_ptr(), None, self.z.data_ptr(), self.corpus.n_tokens,
+                                     self.K, None, self.word_topic.data_ptr(), _lib.stream_handle()), "wd_topic_counts")
+        if self.pg is not None:
+            torch.distributed.all_reduce(self.word_topic, group=self.pg)
+        self.resample(t)
+
+    # ------------------------------------------------------- one sweep
+    def draw(self, t: int, fused_counts: bool = True):
+        self.word_topic.zero_()
+        draw_z_device(self.kernel, self.corpus, self.theta, self.phi, SeededStops(derive_seed(self.seed, 1, t)),
+                      self.lanes, z=self.z, word_topic=self.word_topic if fused_counts else None, err=self.err,
+                      check=False)
+
+    def allreduce_counts(self):
+        if self.pg is not None:
+            self.torch.distributed.all_reduce(self.word_topic, group=self.pg)
+
+    def resample(self, t: int):
+        L = _lib.load()
+        st = _lib.stream_handle()
+        _lib.check(L.wd_resample_phi(self._dt, self.word_topic.data_ptr(), self.V, self.K, self.beta,
+                                     derive_seed(self.seed, 2, t, 1), self.phi.data_ptr(), self.phi.stride(0),
+                                     self._phi_ws.data_ptr(), self._phi_ws.numel(), st), "wd_resample_phi")
+        _lib.check(L.wd_resample_theta(self._dt, self.z.data_ptr(), self.corpus.offsets.data_ptr(),
+                                       self.corpus.n_docs, self.K, self.alpha, derive_seed(self.seed, 2, t, 0),
+                                       self.corpus.doc_base, self.theta.data_ptr(), self.theta.stride(0), st),
+                   "wd_resample_theta")
+
+    def iterate(self, t: int):
+        self.draw(t)
+        self.allreduce_counts()
+        self.resample(t)
+
+    def check_errors(self):
+        raise_for_err(self.err.cpu().numpy().view(np.uint64), _lib.WD_KEYS_MASTER, self.lanes)
+
+    # -------------------------------------------------- log-likelihood
+    def log_likelihood(self) -> float:
+        """lda.py:289-305 on the device (float64 accumulation), summed over ranks."""
+        L = _lib.load()
+        c = self.corpus
+        _lib.check(L.wd_log_likelihood(self._dt, self.theta.data_ptr(), self.theta.stride(0), self.phi.data_ptr(),
+                                       self.phi.stride(0), c.words.data_ptr(), c.token_doc.data_ptr(), c.n_docs,
+                                       c.n_tokens, self.V, self.K, self._ll_out.data_ptr(), self._ll_ws.data_ptr(),
+                                       self._ll_ws.numel(), _lib.stream_handle()), "wd_log_likelihood")
+        out = self._ll_out.clone()
+        if self.pg is not None:
+            self.torch.distributed.all_reduce(out, group=self.pg)
+        return float(out.item())

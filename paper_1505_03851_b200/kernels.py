@@ -1,0 +1,390 @@
+"""Drop-in replacement for the reference's kernel registry (kernels.py:542-555).
+
+Same names, signatures, error types and messages as
+/root/reference/pkg/src/warpdraw/kernels.py; the work runs in the sm_100a
+kernels of libwarpdraw_b200.so:
+
+    draw_z_butterfly   -> wd_draw_z(WD_BUTTERFLY, keys = master index)
+    draw_z_transposed  -> wd_draw_z(WD_PREFIX,    keys = master index)
+    draw_z_basic       -> wd_draw_z(WD_PREFIX,    keys = word position)
+
+z is bit-identical to the reference for float32 and float64 inputs (see
+tests/test_gpu_parity.py).  Two entry levels:
+
+  * the reference signature (host numpy in, ragged int64 lists out);
+  * draw_z_device: device-resident corpus/parameters (DeviceCorpus + torch
+    CUDA tensors), z as an int32 CUDA tensor, optional fused topic counts --
+    the fast path the LDA driver and bench.py use.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .sampling import AllZeroError
+from .warp import Trace, WarpConfig
+
+__all__ = [
+    "StopOutOfRangeError",
+    "SeededStops",
+    "InjectedStops",
+    "PhiloxStops",
+    "DeviceCorpus",
+    "draw_z_device",
+    "draw_z_basic",
+    "draw_z_transposed",
+    "draw_z_butterfly",
+    "KERNELS",
+    "draw_z",
+]
+
+
+class StopOutOfRangeError(ValueError):
+    """A search was handed a stop value outside [0, sum)."""
+
+
+# --- stop randomness providers (kernels.py:42-92) ---
+
+
+class SeededStops:
+    """Fresh hashed stream per (document, master iteration) (kernels.py:42-53).
+
+    On the device the hash is evaluated inline at each stored token's final
+    key, so no redundant redraws are executed.
+    """
+
+    def __init__(self, seed: int):
+        self.seed = int(seed)
+
+    def units(self, m, i, i_master):
+        from .rng import units_for
+
+        return units_for(self.seed, m, i_master)
+
+
+class InjectedStops:
+    """Pre-drawn unit values looked up by (document, word index) (kernels.py:56-92)."""
+
+    def __init__(self, units):
+        self._units = [np.asarray(u, dtype=np.float64) for u in units]
+
+    @classmethod
+    def from_seed(cls, seed: int, lengths) -> "InjectedStops":
+        from .rng import units_for
+
+        return cls([units_for(seed, np.full(int(n), m), np.arange(int(n))) for m, n in enumerate(lengths)])
+
+    @classmethod
+    def from_file(cls, path, lengths) -> "InjectedStops":
+        flat = np.loadtxt(path, dtype=np.float64, ndmin=1)
+        if flat.size != int(np.sum(lengths)):
+            raise ValueError(
+                f"stop file {path} holds {flat.size} values, corpus needs {int(np.sum(lengths))}"
+            )
+        if np.any(flat < 0) or np.any(flat >= 1):
+            raise ValueError("injected values must lie in [0, 1)")
+        out, start = [], 0
+        for n in lengths:
+            out.append(flat[start : start + n])
+            start += n
+        return cls(out)
+
+    def units(self, m, i, i_master):
+        mm = np.atleast_1d(np.asarray(m))
+        ii = np.atleast_1d(np.asarray(i))
+        out = np.zeros(mm.shape, dtype=np.float64)
+        for t in range(mm.size):
+            row = self._units[int(mm.flat[t])]
+            out.flat[t] = row[int(ii.flat[t])] if row.size else 0.0
+        return out
+
+    def flat(self, lengths) -> np.ndarray:
+        """u in CSR token order (doc-major), the device layout."""
+        parts = []
+        for m, n in enumerate(lengths):
+            n = int(n)
+            if n == 0:
+                continue
+            row = self._units[m]
+            parts.append(row[:n] if row.size else np.zeros(n))
+        return np.concatenate(parts) if parts else np.zeros(0)
+
+
+class PhiloxStops:
+    """Opt-in counter-based Philox4x32-10 stream keyed by (seed, doc, word).
+
+    NOT reference-parity (the reference's stream is the SplitMix64/xoshiro
+    hash); provided for users who want a standard counter RNG.
+    """
+
+    def __init__(self, seed: int):
+        self.seed = int(seed)
+
+
+# --- device corpus ---
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+@dataclass
+class DeviceCorpus:
+    """A CSR corpus shard resident in HBM.
+
+    offsets [n_docs+1] int64, words [n_tokens] int32, token_doc [n_tokens]
+    int32, last_key [n_docs] int32 (master-index key of each doc's last
+    word for `lanes`-doc groups).  doc_base is the global id of local doc 0.
+    """
+
+    offsets: object
+    words: object
+    token_doc: object
+    n_docs: int
+    n_tokens: int
+    doc_base: int = 0
+    vocab_size: int | None = None
+    _last_key: dict = field(default_factory=dict)
+
+    @classmethod
+    def from_csr(cls, offsets, words, doc_base: int = 0, vocab_size: int | None = None, device=None):
+        torch = _torch()
+        _lib.require_cuda()
+        dev = device or torch.device("cuda")
+        off = torch.as_tensor(np.asarray(offsets, dtype=np.int64) if not torch.is_tensor(offsets) else offsets,
+                              dtype=torch.int64).to(dev).contiguous()
+        wd = torch.as_tensor(np.asarray(words, dtype=np.int32) if not torch.is_tensor(words) else words,
+                             dtype=torch.int32).to(dev).contiguous()
+        n_docs = off.numel() - 1
+        n_tokens = wd.numel()
+        td = torch.empty(n_tokens, dtype=torch.int32, device=dev)
+        L = _lib.load()
+        _lib.check(L.wd_corpus_prepare(off.data_ptr(), n_docs, n_tokens, int(doc_base), 32, td.data_ptr(), None,
+                                       _lib.stream_handle()), "wd_corpus_prepare")
+        return cls(off, wd, td, n_docs, n_tokens, int(doc_base), vocab_size)
+
+    @classmethod
+    def from_ragged(cls, lengths, words, doc_base: int = 0, vocab_size: int | None = None):
+        lengths = np.asarray(lengths, dtype=np.int64)
+        offsets = np.zeros(lengths.size + 1, dtype=np.int64)
+        np.cumsum(lengths, out=offsets[1:])
+        flat = [np.asarray(words[m], dtype=np.int64)[: int(lengths[m])] for m in range(lengths.size)]
+        flat = np.concatenate(flat).astype(np.int32) if flat else np.zeros(0, np.int32)
+        if flat.size != int(offsets[-1]):
+            raise ValueError("word lists shorter than the document lengths")
+        return cls.from_csr(offsets, flat, doc_base, vocab_size)
+
+    def last_key(self, lanes: int):
+        if lanes not in self._last_key:
+            torch = _torch()
+            lk = torch.empty(max(self.n_docs, 1), dtype=torch.int32, device=self.offsets.device)
+            L = _lib.load()
+            _lib.check(L.wd_corpus_prepare(self.offsets.data_ptr(), self.n_docs, self.n_tokens, self.doc_base,
+                                           int(lanes), None, lk.data_ptr(), _lib.stream_handle()),
+                       "wd_corpus_prepare")
+            self._last_key[lanes] = lk
+        return self._last_key[lanes]
+
+
+_DTYPES = {"float32": _lib.WD_FLOAT32, "float64": _lib.WD_FLOAT64}
+
+
+def _dtype_code(t) -> int:
+    name = str(t.dtype).replace("torch.", "")
+    if name not in _DTYPES:
+        raise TypeError(f"theta/phi must be float32 or float64, got {t.dtype}")
+    return _DTYPES[name]
+
+
+_workspace_cache: dict = {}
+
+
+def _workspace(variant, dtype_code, lanes, K, device):
+    L = _lib.load()
+    nbytes = int(L.wd_workspace_bytes(variant, dtype_code, lanes, int(K)))
+    if nbytes == 0:
+        return None, 0
+    torch = _torch()
+    key = (str(device), variant)
+    buf = _workspace_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _workspace_cache[key] = buf
+    return buf, nbytes
+
+
+_KERNEL_SPEC = {
+    # name: (variant, key rule, requires M % W == 0)
+    "basic": (_lib.WD_PREFIX, _lib.WD_KEYS_POSITION, False),
+    "transposed": (_lib.WD_PREFIX, _lib.WD_KEYS_MASTER, True),
+    "butterfly": (_lib.WD_BUTTERFLY, _lib.WD_KEYS_MASTER, True),
+}
+
+
+def _token_positions(corpus: DeviceCorpus):
+    """Host (m, i) of every token in CSR order (only for generic stop providers)."""
+    off = corpus.offsets.cpu().numpy()
+    lengths = np.diff(off)
+    m = np.repeat(np.arange(corpus.n_docs), lengths)
+    i = np.arange(corpus.n_tokens) - np.repeat(off[:-1], lengths)
+    return m, i, lengths
+
+
+def _stop_args(stops, corpus: DeviceCorpus, key_rule: int, lanes: int, device):
+    """Map a stops provider to (mode, seed, units tensor)."""
+    torch = _torch()
+    if isinstance(stops, SeededStops):
+        return _lib.WD_STOPS_SEEDED, stops.seed, None
+    if isinstance(stops, PhiloxStops):
+        return _lib.WD_STOPS_PHILOX, stops.seed, None
+    if isinstance(stops, InjectedStops):
+        lengths = np.diff(corpus.offsets.cpu().numpy())
+        flat = stops.flat(lengths)
+        return _lib.WD_STOPS_UNITS, 0, torch.from_numpy(np.ascontiguousarray(flat)).to(device)
+    if torch.is_tensor(stops):  # u per token, float64, CSR order
+        return _lib.WD_STOPS_UNITS, 0, stops.to(device=device, dtype=torch.float64).contiguous()
+    if hasattr(stops, "units"):
+        # duck-typed provider: evaluate .units at each stored token's final
+        # key (kernels.py:520-536 master-index rule) on the host
+        m, i, lengths = _token_positions(corpus)
+        i_master = i.copy()
+        if key_rule == _lib.WD_KEYS_MASTER and corpus.n_docs:
+            gm = corpus.doc_base + np.arange(corpus.n_docs)
+            q = gm // lanes
+            gmax = np.zeros(q.max() + 1, dtype=np.int64)
+            np.maximum.at(gmax, q, lengths)
+            last = i == lengths[m] - 1
+            i_master[last] = gmax[q[m[last]]] - 1
+        u = np.asarray(stops.units(corpus.doc_base + m, i, i_master), dtype=np.float64)
+        return _lib.WD_STOPS_UNITS, 0, torch.from_numpy(np.ascontiguousarray(u)).to(device)
+    raise TypeError(f"unsupported stops provider {type(stops).__name__}")
+
+
+def raise_for_err(err_host, key_rule: int, lanes: int):
+    allzero, stop_bad = int(err_host[0]), int(err_host[1])
+    if stop_bad:
+        raise StopOutOfRangeError("stop values must lie in [0, sum)")
+    if allzero != _lib.ERR_NONE:
+        if key_rule == _lib.WD_KEYS_POSITION:
+            m, i = allzero >> 32, allzero & 0xFFFFFFFF
+            raise AllZeroError(f"document {m}, word {i}: all products are zero")
+        q, r = allzero >> 40, allzero & 0xFF
+        raise AllZeroError(f"document {q * lanes + r}: all products are zero")
+
+
+def draw_z_device(kernel: str, corpus: DeviceCorpus, theta, phi, stops, lanes: int = 32, *, z=None,
+                  word_topic=None, doc_topic=None, err=None, check: bool = True, stream=None):
+    """Device-resident draw.  theta [n_docs, K], phi [V, K] CUDA tensors
+    (float32 or float64, same dtype, row stride = leading dim).  Returns z
+    (int32 CUDA tensor, CSR token order).  word_topic / doc_topic (int32) are
+    incremented in the same kernel when given.  check=False skips the host
+    synchronisation on the error word (err must then be supplied and
+    inspected by the caller, e.g. with raise_for_err)."""
+    torch = _torch()
+    if kernel not in _KERNEL_SPEC:
+        raise ValueError(f"unknown kernel {kernel!r}; pick one of {sorted(_KERNEL_SPEC)}")
+    variant, key_rule, needs_pad = _KERNEL_SPEC[kernel]
+    if needs_pad and (corpus.n_docs % lanes or corpus.doc_base % lanes):
+        raise ValueError("document count must be a multiple of the lane count (pad upstream)")
+    _lib.require_cuda()
+    if theta.dtype != phi.dtype:
+        phi = phi.to(theta.dtype)
+    if theta.stride(-1) != 1 or phi.stride(-1) != 1:
+        raise ValueError("theta/phi rows must be contiguous")
+    K = int(theta.shape[1])
+    if int(phi.shape[1]) != K:
+        raise ValueError("theta and phi disagree on the topic count")
+    if theta.shape[0] < corpus.n_docs:
+        raise ValueError("theta has fewer rows than the corpus has documents")
+    dev = theta.device
+    dt = _dtype_code(theta)
+    mode, seed, units = _stop_args(stops, corpus, key_rule, lanes, dev)
+    if mode == _lib.WD_STOPS_UNITS and units.numel() < corpus.n_tokens:
+        raise ValueError("units do not cover every token")
+    if z is None:
+        z = torch.empty(corpus.n_tokens, dtype=torch.int32, device=dev)
+    own_err = err is None
+    if own_err:
+        err = torch.empty(2, dtype=torch.int64, device=dev)
+    last_key = corpus.last_key(lanes) if (mode == _lib.WD_STOPS_SEEDED and key_rule == _lib.WD_KEYS_MASTER) else None
+    ws, ws_bytes = _workspace(variant, dt, lanes, K, dev)
+    L = _lib.load()
+    _lib.check(
+        L.wd_draw_z(variant, dt, int(lanes), theta.data_ptr(), theta.stride(0), phi.data_ptr(), phi.stride(0), K,
+                    corpus.offsets.data_ptr(), corpus.words.data_ptr(), corpus.token_doc.data_ptr(),
+                    _lib.ptr(last_key), corpus.n_docs, corpus.n_tokens, corpus.doc_base, mode, key_rule,
+                    int(seed) & ((1 << 64) - 1), _lib.ptr(units), None, z.data_ptr(), _lib.ptr(word_topic),
+                    _lib.ptr(doc_topic), err.data_ptr(), _lib.ptr(ws), ws_bytes, _lib.stream_handle(stream)),
+        "wd_draw_z")
+    if check:
+        raise_for_err(err.cpu().numpy().view(np.uint64), key_rule, lanes)
+    return z
+
+
+def _to_host_ragged(z_dev, N):
+    zf = z_dev.cpu().numpy().astype(np.int64)
+    out, start = [], 0
+    for n in N:
+        n = int(n)
+        out.append(zf[start : start + n])
+        start += n
+    return out
+
+
+def _host_call(kernel, N, theta, phi, w, lanes, stops, trace, threads, step_hook):
+    torch = _torch()
+    if step_hook is not None:
+        raise NotImplementedError("step_hook is an emulator instrumentation hook; not available on the device path")
+    theta = np.asarray(theta)
+    phi = np.asarray(phi)
+    if theta.dtype not in (np.float32, np.float64):
+        theta = theta.astype(np.float64)
+    N = np.asarray(N, dtype=np.int64)
+    M = theta.shape[0] if kernel != "basic" else len(N)
+    if kernel != "basic" and M % lanes:
+        raise ValueError("document count must be a multiple of the lane count (pad upstream)")
+    _lib.require_cuda()
+    corpus = DeviceCorpus.from_ragged(N, w)
+    dev = torch.device("cuda")
+    th = torch.from_numpy(np.ascontiguousarray(theta)).to(dev)
+    ph = torch.from_numpy(np.ascontiguousarray(phi.astype(theta.dtype, copy=False))).to(dev)
+    z = draw_z_device(kernel, corpus, th, ph, stops, lanes)
+    return _to_host_ragged(z, N)
+
+
+def draw_z_basic(N, theta, phi, w, stops) -> list:
+    """Sequential-order prefix table per word (kernels.py:380-401), on the GPU."""
+    return _host_call("basic", N, theta, phi, w, 32, stops, None, 1, None)
+
+
+def draw_z_transposed(N, theta, phi, w, config: WarpConfig, stops, trace: Trace | None = None, threads: int = 1,
+                      step_hook=None) -> list:
+    """The paper's full prefix-sum-table kernel (kernels.py:428-484), on the GPU."""
+    return _host_call("transposed", N, theta, phi, w, config.lanes, stops, trace, threads, step_hook)
+
+
+def draw_z_butterfly(N, theta, phi, w, config: WarpConfig, stops, trace: Trace | None = None, threads: int = 1,
+                     step_hook=None) -> list:
+    """Butterfly-patterned partial sums (kernels.py:487-539), on the GPU."""
+    return _host_call("butterfly", N, theta, phi, w, config.lanes, stops, trace, threads, step_hook)
+
+
+KERNELS = {
+    "basic": draw_z_basic,
+    "transposed": draw_z_transposed,
+    "butterfly": draw_z_butterfly,
+}
+
+
+def draw_z(kernel: str, N, theta, phi, w, config: WarpConfig, stops, **kwargs):
+    """Dispatch a kernel by name with a uniform signature (kernels.py:549-555)."""
+    if kernel not in KERNELS:
+        raise ValueError(f"unknown kernel {kernel!r}; pick one of {sorted(KERNELS)}")
+    if kernel == "basic":
+        return draw_z_basic(N, theta, phi, w, stops)
+    return KERNELS[kernel](N, theta, phi, w, config, stops, **kwargs)

@@ -1,0 +1,137 @@
+"""Standalone samplers: the reference's SAMPLERS registry (bench.py:118-154)
+plus the batched independent-row API used by the K sweep (BASELINE configs[1]).
+
+    sample_butterfly(weights, n, seed, lanes=8)   bench.py:129-147, on the GPU
+    sample_prefix(weights, n, seed, lanes=8)      same u stream, prefix table
+    sample_rows(weights[n, K], seed, ...)         one independent row per draw
+
+The u stream is units_for(derive_seed(seed, 6), draw_id) exactly as in
+bench.py:141-143; results are bit-identical to the reference.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .kernels import StopOutOfRangeError
+from .rng import derive_seed
+from .sampling import AllZeroError
+
+_VARIANTS = {"butterfly": _lib.WD_BUTTERFLY, "prefix": _lib.WD_PREFIX}
+
+
+def _dtype_code(t):
+    import torch
+
+    if t.dtype == torch.float32:
+        return _lib.WD_FLOAT32
+    if t.dtype == torch.float64:
+        return _lib.WD_FLOAT64
+    raise TypeError(f"weights must be float32 or float64, got {t.dtype}")
+
+
+def sample_rows(weights, seed: int | None = None, *, lanes: int = 32, variant: str = "butterfly", row_base: int = 0,
+                units=None, stops=None, out=None, n: int | None = None, err=None, check: bool = True, stream=None,
+                raw_seed: int | None = None):
+    """Draw one index per row of `weights` ([n, K] CUDA tensor, float32/64).
+
+    A 1-D weights tensor is one shared vector; pass n for the number of draws.
+    Row id = row_base + i; u = units_for(derive_seed(seed, 6), id) unless
+    `units` (float64 per row) or `stops` (explicit, weights dtype) are given.
+    Returns an int32 CUDA tensor.  Rows summing to zero raise AllZeroError
+    when check=True (the reference's search returns index K-1 for them).
+    """
+    import torch
+
+    _lib.require_cuda()
+    if variant not in _VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}")
+    if weights.dim() == 1:
+        if n is None:
+            raise ValueError("a shared weight vector needs n")
+        ld = 0
+        K = int(weights.shape[0])
+    else:
+        n, K = int(weights.shape[0]), int(weights.shape[1])
+        if weights.stride(-1) != 1:
+            raise ValueError("weight rows must be contiguous")
+        ld = weights.stride(0)
+    dt = _dtype_code(weights)
+    dev = weights.device
+    mode, sd, u_t, s_t = _lib.WD_STOPS_SEEDED, 0, None, None
+    if stops is not None:
+        mode = _lib.WD_STOPS_EXPLICIT
+        s_t = torch.as_tensor(stops, dtype=weights.dtype).to(dev).contiguous()
+    elif units is not None:
+        mode = _lib.WD_STOPS_UNITS
+        u_t = torch.as_tensor(units, dtype=torch.float64).to(dev).contiguous()
+    else:
+        sd = raw_seed if raw_seed is not None else derive_seed(int(seed), 6)
+    if out is None:
+        out = torch.empty(n, dtype=torch.int32, device=dev)
+    own_err = err is None
+    if own_err:
+        err = torch.empty(2, dtype=torch.int64, device=dev)
+    L = _lib.load()
+    v = _VARIANTS[variant]
+    nbytes = int(L.wd_workspace_bytes(v, dt, int(lanes), K))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev) if nbytes else None
+    _lib.check(L.wd_sample_rows(v, dt, int(lanes), weights.data_ptr(), ld, n, K, int(row_base), mode,
+                                int(sd) & ((1 << 64) - 1), _lib.ptr(u_t), _lib.ptr(s_t), out.data_ptr(),
+                                err.data_ptr(), _lib.ptr(ws), nbytes, _lib.stream_handle(stream)),
+               "wd_sample_rows")
+    if check:
+        e = err.cpu().numpy().view(np.uint64)
+        if int(e[1]):
+            raise StopOutOfRangeError("stop values must lie in [0, sum)")
+        if int(e[0]) != _lib.ERR_NONE and stops is None:
+            raise AllZeroError(f"row {int(e[0])}: all weights are zero")
+    return out
+
+
+def _shared(weights, n, seed, lanes, variant):
+    import torch
+
+    w = np.asarray(weights, dtype=np.float64)
+    if n <= 0:
+        return np.zeros(0, dtype=np.int64)
+    wt = torch.from_numpy(np.ascontiguousarray(w)).cuda()
+    # bench.py:129-147 builds no AllZero check; the search returns K-1 there
+    idx = sample_rows(wt, seed, lanes=lanes, variant=variant, n=int(n), check=False)
+    return idx.cpu().numpy().astype(np.int64)
+
+
+def sample_butterfly(weights, n: int, seed: int, lanes: int = 8) -> np.ndarray:
+    """Draw through the butterfly table and search (bench.py:129-147)."""
+    return _shared(weights, n, seed, lanes, "butterfly")
+
+
+def sample_prefix(weights, n: int, seed: int, lanes: int = 8) -> np.ndarray:
+    """Same u stream through the full prefix-sum table (the paper's baseline)."""
+    return _shared(weights, n, seed, lanes, "prefix")
+
+
+SAMPLERS = {
+    "butterfly": sample_butterfly,
+    "prefix": sample_prefix,
+}
+
+
+def chi_square(observed, expected) -> tuple[float, int]:
+    """Pearson statistic and degrees of freedom (bench.py:30-50)."""
+    obs = np.asarray(observed, dtype=np.float64)
+    exp = np.asarray(expected, dtype=np.float64)
+    if obs.shape != exp.shape or obs.ndim != 1 or obs.size < 2:
+        raise ValueError("need matching 1-D bins, at least two")
+    if np.any(exp <= 0):
+        raise ValueError("expected probabilities must be positive")
+    n = obs.sum()
+    stat = float(np.sum((obs - exp * n) ** 2 / (exp * n)))
+    return stat, obs.size - 1
+
+
+def chi_square_critical(dof: int, significance: float = 0.001) -> float:
+    from scipy import stats
+
+    return float(stats.chi2.ppf(1.0 - significance, dof))

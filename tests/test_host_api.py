@@ -1,0 +1,135 @@
+"""CPU-side checks: the C-ABI library loads and exports every declared
+symbol, the host logic of the API mirror matches the reference semantics,
+and the product path refuses to run without CUDA (no CPU fallback)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1505_03851_b200 as wd
+from paper_1505_03851_b200 import _lib
+from oracle import oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    text = open(os.path.join(ROOT, "include", "warpdraw_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:const char\*|int|size_t)\s+(wd_\w+)\(", text, re.M)))
+
+
+def test_header_declares_the_bound_exports():
+    assert _declared_symbols() == sorted(_lib.EXPORTS)
+
+
+def test_library_loads_and_exports_every_symbol():
+    from paper_1505_03851_b200 import build
+
+    path = build.build()
+    L = ctypes.CDLL(path)
+    for name in _declared_symbols():
+        assert hasattr(L, name), name
+    h = _lib.load(path)
+    assert h.wd_abi_version() == 1
+    assert h.wd_status_string(0) == b"ok"
+
+
+def test_invalid_arguments_rejected_without_gpu():
+    L = _lib.load()
+    # validation happens before any device work
+    assert L.wd_draw_z(0, 0, 3, None, 0, None, 0, 8, None, None, None, None, 0, 0, 0, 0, 0, 0, None, None,
+                       None, None, None, None, None, 0, None) == 1  # lanes=3
+    assert L.wd_units(0, 3, None, None, 1, None, None) == 1
+    assert L.wd_sample_rows(0, 2, 32, None, 0, 1, 8, 0, 0, 0, None, None, None, None, None, 0, None) == 1
+
+
+def test_product_path_has_no_cpu_fallback():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(_lib.NativeLibraryError):
+        wd.sample_rows(torch.ones((4, 4)), 1)
+    with pytest.raises(_lib.NativeLibraryError):
+        wd.draw_z("butterfly", [1] * 8, np.ones((8, 4)), np.ones((2, 4)), [np.zeros(1, np.int64)] * 8,
+                  wd.WarpConfig(lanes=8), wd.SeededStops(1))
+    with pytest.raises(_lib.NativeLibraryError):
+        wd.units_for(1, np.arange(3))
+
+
+def test_host_seed_plumbing_matches_oracle():
+    gen = np.random.default_rng(0)
+    for _ in range(200):
+        s = int(gen.integers(0, 2**63))
+        ks = [int(k) for k in gen.integers(-(2**40), 2**40, size=int(gen.integers(0, 4)))]
+        assert wd.derive_seed(s, *ks) == O.derive_seed(s, *ks)
+        assert wd.unit_for(s, *ks) == O.units(s, *[[k] for k in ks])[0] if len(ks) <= 3 else True
+    assert wd.derive_seed(7, 1, 0) == 0xB5D8C8503FA207B1
+
+
+def test_warp_config_validation():
+    with pytest.raises(ValueError):
+        wd.WarpConfig(lanes=3)
+    with pytest.raises(ValueError):
+        wd.WarpConfig(lanes=128)
+    with pytest.raises(ValueError):
+        wd.WarpConfig(elem_size=2)
+    assert wd.WarpConfig(lanes=64).log2_lanes == 6
+
+
+def test_corpus_padding_and_csr():
+    c = wd.Corpus(vocab_size=5, lengths=np.array([2, 0, 3]), words=[np.array([1, 2]), np.zeros(0), np.array([4, 0, 1])])
+    p = c.padded(8)
+    assert p.n_docs == 8 and p.padding == 5 and p.n_real_docs == 3
+    off, words = p.csr()
+    np.testing.assert_array_equal(off, [0, 2, 2, 5, 5, 5, 5, 5, 5])
+    np.testing.assert_array_equal(words, [1, 2, 4, 0, 1])
+    assert c.padded(3) is c
+
+
+def test_injected_stops_from_file(tmp_path):
+    lengths = [2, 0, 1]
+    path = tmp_path / "stops.txt"
+    path.write_text("0.1\n0.2\n0.3\n")
+    stops = wd.InjectedStops.from_file(path, lengths)
+    np.testing.assert_array_equal(stops.units(np.array([0, 0, 2]), np.array([0, 1, 0]), None), [0.1, 0.2, 0.3])
+    np.testing.assert_array_equal(stops.flat(lengths), [0.1, 0.2, 0.3])
+    path.write_text("0.1\n")
+    with pytest.raises(ValueError, match="holds 1"):
+        wd.InjectedStops.from_file(path, lengths)
+    path.write_text("0.1\n0.2\n1.0\n")
+    with pytest.raises(ValueError, match=r"\[0, 1\)"):
+        wd.InjectedStops.from_file(path, lengths)
+
+
+def test_corpus_file_roundtrip(tmp_path):
+    c = wd.Corpus(vocab_size=9, lengths=np.array([3, 1]), words=[np.array([1, 8, 2]), np.array([0])])
+    p = tmp_path / "c.txt"
+    wd.save_corpus(c, p)
+    d = wd.load_corpus(p)
+    assert d.vocab_size == 9
+    np.testing.assert_array_equal(d.lengths, [3, 1])
+    p.write_text("#2 5\n1 2\n7\n")
+    with pytest.raises(wd.WordIdOutOfRangeError):
+        wd.load_corpus(p)
+    p.write_text("1 x\n")
+    with pytest.raises(wd.CorpusParseError):
+        wd.load_corpus(p)
+
+
+def test_init_assignments_matches_reference_stream():
+    c = wd.Corpus(vocab_size=5, lengths=np.array([4, 0, 2]), words=[np.zeros(4), np.zeros(0), np.zeros(2)])
+    z = wd.init_assignments(c, 7, 11)
+    gen = np.random.default_rng(O.derive_seed(11, 0))
+    exp = [gen.integers(0, 7, size=n) for n in (4, 0, 2)]
+    for a, b in zip(z, exp):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_chi_square():
+    stat, dof = wd.chi_square([10, 10], [0.5, 0.5])
+    assert stat == 0.0 and dof == 1
+    assert abs(wd.chi_square_critical(18) - 42.3124) < 1e-3
