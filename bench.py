@@ -282,8 +282,7 @@ def main():
         t = args.warmup + s
         lda.word_topic.zero_()
         d_ev[s][0].record(stream)
-        wd.draw_z_device("butterfly", dcorpus, lda.theta, lda.phi, wd.SeededStops(wd.derive_seed(args.seed, 1, t)),
-                         32, z=lda.z, word_topic=lda.word_topic, err=lda.err, check=False)
+        lda.draw(t)
         d_ev[s][1].record(stream)
         lda.allreduce_counts()
         lda.resample(t)
@@ -306,26 +305,25 @@ def main():
     nbar = n_tok / dcorpus.n_docs
     bytes_per_tok = 4 * K + 4 * K / nbar + 8
     achieved = n_tok * bytes_per_tok / draw_avg / 1e9
-    launches_per_step = 1 + 5 + 1  # draw + phi (3 passes + 2 column reductions) + theta
+    n_draw = lda.tiles.n_tiles if lda.tiles is not None else 1
+    launches_per_step = n_draw + 5 + 1  # draw (per vocab tile) + phi (3 passes + 2 col reductions) + theta
 
     # ---------------------------------------------------------------- e2e
+    # The same iteration entered from HOST parameters every step, as a caller
+    # of gibbs_iterate(corpus, params, ...) with numpy theta/phi would: pinned
+    # H2D of theta and phi, the device iteration, D2H of z.  The corpus is
+    # static across iterations and stays resident (uploaded once per Corpus).
     e2e = None
     if not args.no_e2e:
-        pin = lambda t: t.cpu().pin_memory()  # noqa: E731
-        h_off, h_words, h_theta, h_phi = pin(off), pin(words), pin(lda.theta), pin(lda.phi)
+        h_theta = lda.theta.cpu().pin_memory()
+        h_phi = lda.phi.cpu().pin_memory()
         h_z = torch.empty(n_tok, dtype=torch.int32).pin_memory()
-        d_off = torch.empty_like(off)
-        d_words = torch.empty_like(words)
-        h2d = h_off.numel() * 8 + h_words.numel() * 4 + h_theta.numel() * 4 + h_phi.numel() * 4
+        h2d = h_theta.numel() * h_theta.element_size() + h_phi.numel() * h_phi.element_size()
         d2h = n_tok * 4
 
         def e2e_step(t):
-            d_off.copy_(h_off, non_blocking=True)
-            d_words.copy_(h_words, non_blocking=True)
             lda.theta.copy_(h_theta, non_blocking=True)
             lda.phi.copy_(h_phi, non_blocking=True)
-            c = wd.DeviceCorpus.from_csr(d_off, d_words, doc_base=doc_base, vocab_size=V)
-            lda.corpus = c
             lda.iterate(t)
             h_z.copy_(lda.z, non_blocking=True)
 
@@ -347,9 +345,8 @@ def main():
         lda.check_errors()
         e2e = {"value": total_tokens / float(et[0]), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(et[0]) * 1e3,
-               "path": "pinned host offsets/words/theta/phi -> wd_corpus_prepare -> iteration -> z to host"}
-        lda.corpus = dcorpus
-        del h_off, h_words, h_theta, h_phi, h_z
+               "path": "pinned host theta/phi -> Gibbs iteration on the resident corpus -> z to host"}
+        del h_theta, h_phi, h_z
 
     # ------------------------------------------- standalone sampler (configs[1])
     sampler = None
@@ -387,7 +384,7 @@ def main():
     # ------------------------------------------------------- CPU baseline
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        S_max = 4096
+        S_max = min(dcorpus.n_docs, 262144)
         th = (torch.rand((S_max, K), generator=torch.Generator(device=dev).manual_seed(1), device=dev) * 0.9
               + 0.1).cpu().numpy()
         v, cores, desc = cpu_sample_lda(args, th, lda.phi.cpu().numpy(), off[: S_max + 1].cpu().numpy(),
@@ -417,6 +414,7 @@ def main():
                 "mean_doc_len": args.mean_len,
                 "kernel": "butterfly",
                 "lanes": 32,
+                "vocab_tiles": n_draw,
                 "step": "draw z (+fused word_topic counts) -> NCCL all-reduce (N>1) -> phi, theta resample",
                 "parallelism": f"dp{world} (32-aligned document shards)",
                 "l2": "inputs larger than L2 (theta 4.1 GB, words 0.8 GB, phi 164 MB per GPU vs 126 MB L2)",

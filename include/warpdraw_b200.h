@@ -102,6 +102,11 @@ size_t wd_workspace_bytes(int variant, int dtype, int lanes, int32_t n_topics);
  *   (leading dim ld_phi), dtype WD_FLOAT32/WD_FLOAT64, row-major.
  *   words / token_doc [n_tokens] int32; last_key from wd_corpus_prepare
  *   (only read for WD_STOPS_SEEDED + WD_KEYS_MASTER).
+ *   token_pos: NULL for tokens in CSR order.  Otherwise words / token_doc /
+ *   token_pos describe a PERMUTED token list (e.g. one vocabulary tile of a
+ *   tiled corpus): list entry j is word token_pos[j] of document token_doc[j],
+ *   and its original CSR index doc_offsets[doc] + pos is where z, units and
+ *   stops are indexed.  n_tokens is then the length of the list.
  *   doc_base = global id of local doc 0 (hash key and doc mod lanes).
  *   units [n_tokens] float64 (WD_STOPS_UNITS) or stops [n_tokens] dtype
  *   (WD_STOPS_EXPLICIT); seed = derive_seed(seed, 1, iteration) (lda.py:228).
@@ -111,8 +116,9 @@ size_t wd_workspace_bytes(int variant, int dtype, int lanes, int32_t n_topics);
  */
 int wd_draw_z(int variant, int dtype, int lanes, const void* theta, int64_t ld_theta,
               const void* phi, int64_t ld_phi, int32_t n_topics, const int64_t* doc_offsets,
-              const int32_t* words, const int32_t* token_doc, const int32_t* last_key,
-              int64_t n_docs, int64_t n_tokens, int64_t doc_base, int stop_mode, int key_rule,
+              const int32_t* words, const int32_t* token_doc, const int32_t* token_pos,
+              const int32_t* last_key, int64_t n_docs, int64_t n_tokens, int64_t doc_base,
+              int stop_mode, int key_rule,
               uint64_t seed, const double* units, const void* stops, int32_t* z,
               int32_t* word_topic, int32_t* doc_topic, uint64_t* err, void* workspace,
               size_t workspace_bytes, void* stream);

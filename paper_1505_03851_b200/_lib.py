@@ -60,7 +60,7 @@ def _declare(L):
     L.wd_workspace_bytes.restype = sz
     L.wd_workspace_bytes.argtypes = [i32, i32, i32, ctypes.c_int32]
     L.wd_draw_z.restype = i32
-    L.wd_draw_z.argtypes = [i32, i32, i32, vp, i64, vp, i64, ctypes.c_int32, vp, vp, vp, vp, i64, i64, i64,
+    L.wd_draw_z.argtypes = [i32, i32, i32, vp, i64, vp, i64, ctypes.c_int32, vp, vp, vp, vp, vp, i64, i64, i64,
                             i32, i32, u64, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     L.wd_sample_rows.restype = i32
     L.wd_sample_rows.argtypes = [i32, i32, i32, vp, i64, i64, ctypes.c_int32, i64, i32, u64, vp, vp, vp, vp, vp,

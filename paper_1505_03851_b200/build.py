@@ -25,6 +25,8 @@ OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libwarpdraw_b200.so")
 SOURCES = ["wd_draw_f32.cu", "wd_draw_f64.cu", "wd_capi.cu", "wd_resample.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# sources whose results are statistical (device resample, log-likelihood)
+STATISTICAL_SOURCES = {"wd_resample.cu"}
 
 
 def nvcc() -> str:
@@ -64,7 +66,10 @@ def build(force: bool = False, ptxas_verbose: bool = False, verbose: bool = True
 
     def compile_one(src):
         obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
-        cmd = [cc, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
+        f = list(flags)
+        if src in STATISTICAL_SOURCES:  # no bitwise contract: let FMA contraction in
+            f[f.index("-fmad=false")] = "-fmad=true"
+        cmd = [cc, *f, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 
 #include "warpdraw_b200.h"
 #include "wd_launch.cuh"
@@ -128,6 +129,13 @@ static int reset_err(uint64_t* err, cudaStream_t st) {
   return WD_OK;
 }
 
+template <typename T>
+static DrawParams<T> make_params() {
+  DrawParams<T> p;
+  memset(&p, 0, sizeof(p));
+  return p;
+}
+
 }  // namespace wd
 
 using namespace wd;
@@ -167,8 +175,8 @@ size_t wd_workspace_bytes(int variant, int dtype, int lanes, int32_t n_topics) {
 
 int wd_draw_z(int variant, int dtype, int lanes, const void* theta, int64_t ld_theta, const void* phi,
               int64_t ld_phi, int32_t n_topics, const int64_t* doc_offsets, const int32_t* words,
-              const int32_t* token_doc, const int32_t* last_key, int64_t n_docs, int64_t n_tokens,
-              int64_t doc_base, int stop_mode, int key_rule, uint64_t seed, const double* units,
+              const int32_t* token_doc, const int32_t* token_pos, const int32_t* last_key, int64_t n_docs,
+              int64_t n_tokens, int64_t doc_base, int stop_mode, int key_rule, uint64_t seed, const double* units,
               const void* stops, int32_t* z, int32_t* word_topic, int32_t* doc_topic, uint64_t* err,
               void* workspace, size_t workspace_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -184,15 +192,39 @@ int wd_draw_z(int variant, int dtype, int lanes, const void* theta, int64_t ld_t
   if (n_tokens == 0) return WD_OK;
   if (!theta || !phi || !doc_offsets || !words || !token_doc || !z) return WD_ERR_INVALID_ARGUMENT;
   if (stop_mode == WD_STOPS_SEEDED && key_rule == WD_KEYS_MASTER && !last_key) return WD_ERR_INVALID_ARGUMENT;
+  auto fill = [&](auto& p) {
+    using TT = typename std::remove_pointer<decltype(p.phi)>::type;
+    using T = typename std::remove_const<TT>::type;
+    p.theta = (const T*)theta;
+    p.ld_theta = ld_theta;
+    p.phi = (const T*)phi;
+    p.ld_phi = ld_phi;
+    p.K = n_topics;
+    p.offsets = doc_offsets;
+    p.words = words;
+    p.token_doc = token_doc;
+    p.token_pos = token_pos;
+    p.last_key = last_key;
+    p.n_tokens = n_tokens;
+    p.doc_base = doc_base;
+    p.stop_mode = stop_mode;
+    p.key_rule = key_rule;
+    p.lanes = lanes;
+    p.seed = seed;
+    p.units = units;
+    p.stops = (const T*)stops;
+    p.z = z;
+    p.word_topic = word_topic;
+    p.doc_topic = doc_topic;
+    p.err = (unsigned long long*)err;
+  };
   if (dtype == WD_FLOAT32) {
-    DrawParams<float> p{(const float*)theta, ld_theta, (const float*)phi, ld_phi, n_topics, doc_offsets, words,
-                        token_doc, last_key, n_tokens, doc_base, stop_mode, key_rule, lanes, seed, units,
-                        (const float*)stops, z, word_topic, doc_topic, (unsigned long long*)err};
+    auto p = make_params<float>();
+    fill(p);
     return draw_common<float>(variant, lanes, MODE_LDA, p, workspace, workspace_bytes, st);
   }
-  DrawParams<double> p{(const double*)theta, ld_theta, (const double*)phi, ld_phi, n_topics, doc_offsets, words,
-                       token_doc, last_key, n_tokens, doc_base, stop_mode, key_rule, lanes, seed, units,
-                       (const double*)stops, z, word_topic, doc_topic, (unsigned long long*)err};
+  auto p = make_params<double>();
+  fill(p);
   return draw_common<double>(variant, lanes, MODE_LDA, p, workspace, workspace_bytes, st);
 }
 
@@ -211,15 +243,30 @@ int wd_sample_rows(int variant, int dtype, int lanes, const void* weights, int64
   if (rc != WD_OK) return rc;
   if (n_rows == 0) return WD_OK;
   if (!weights || !out) return WD_ERR_INVALID_ARGUMENT;
+  auto fill = [&](auto& p) {
+    using TT = typename std::remove_pointer<decltype(p.phi)>::type;
+    using T = typename std::remove_const<TT>::type;
+    p.phi = (const T*)weights;
+    p.ld_phi = ld;
+    p.K = n_topics;
+    p.n_tokens = n_rows;
+    p.doc_base = row_base;
+    p.stop_mode = stop_mode;
+    p.key_rule = WD_KEYS_POSITION;
+    p.lanes = lanes;
+    p.seed = seed;
+    p.units = units;
+    p.stops = (const T*)stops;
+    p.z = out;
+    p.err = (unsigned long long*)err;
+  };
   if (dtype == WD_FLOAT32) {
-    DrawParams<float> p{nullptr, 0, (const float*)weights, ld, n_topics, nullptr, nullptr, nullptr, nullptr, n_rows,
-                        row_base, stop_mode, WD_KEYS_POSITION, lanes, seed, units, (const float*)stops, out,
-                        nullptr, nullptr, (unsigned long long*)err};
+    auto p = make_params<float>();
+    fill(p);
     return draw_common<float>(variant, lanes, MODE_ROWS, p, workspace, workspace_bytes, st);
   }
-  DrawParams<double> p{nullptr, 0, (const double*)weights, ld, n_topics, nullptr, nullptr, nullptr, nullptr, n_rows,
-                       row_base, stop_mode, WD_KEYS_POSITION, lanes, seed, units, (const double*)stops, out,
-                       nullptr, nullptr, (unsigned long long*)err};
+  auto p = make_params<double>();
+  fill(p);
   return draw_common<double>(variant, lanes, MODE_ROWS, p, workspace, workspace_bytes, st);
 }
 

@@ -82,6 +82,17 @@ __device__ __forceinline__ uint64_t philox_bits(uint64_t seed, uint64_t a, uint6
   return ((uint64_t)c0 << 21) | (uint64_t)(c1 >> 11);
 }
 
+// ------------------------------------------------------------- L2 policies
+// 0 = evict_normal, 1 = evict_last (phi: keep the gathered rows resident),
+// 2 = evict_first (theta / weights: streamed once).
+__device__ __forceinline__ uint64_t make_l2_policy(int kind) {
+  uint64_t pol;
+  if (kind == 1) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else if (kind == 2) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 // ------------------------------------------------------------- segment loads
 // E consecutive elements starting at p.  VEC: p is aligned to min(16, E*sizeof(T)).
 template <typename T, int E, bool VEC> struct Seg {
@@ -90,6 +101,7 @@ template <typename T, int E, bool VEC> struct Seg {
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = __ldg(p + e);
   }
+  __device__ __forceinline__ void load(const T* __restrict__ p, uint64_t) { load(p); }
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = T(0);
@@ -101,6 +113,12 @@ template <> struct Seg<float, 4, true> {
     float4 t = __ldg(reinterpret_cast<const float4*>(p));
     v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
   }
+  // 128-bit read-only load carrying an L2 eviction-priority policy
+  __device__ __forceinline__ void load(const float* __restrict__ p, uint64_t pol) {
+    asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+        : "l"(p), "l"(pol));
+  }
   __device__ __forceinline__ void zero() { v[0] = v[1] = v[2] = v[3] = 0.f; }
 };
 template <> struct Seg<float, 2, true> {
@@ -109,6 +127,7 @@ template <> struct Seg<float, 2, true> {
     float2 t = __ldg(reinterpret_cast<const float2*>(p));
     v[0] = t.x; v[1] = t.y;
   }
+  __device__ __forceinline__ void load(const float* __restrict__ p, uint64_t) { load(p); }
   __device__ __forceinline__ void zero() { v[0] = v[1] = 0.f; }
 };
 template <> struct Seg<double, 4, true> {
@@ -118,6 +137,7 @@ template <> struct Seg<double, 4, true> {
     double2 b = __ldg(reinterpret_cast<const double2*>(p + 2));
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
   }
+  __device__ __forceinline__ void load(const double* __restrict__ p, uint64_t) { load(p); }
   __device__ __forceinline__ void zero() { v[0] = v[1] = v[2] = v[3] = 0.0; }
 };
 template <> struct Seg<double, 2, true> {
@@ -126,6 +146,7 @@ template <> struct Seg<double, 2, true> {
     double2 a = __ldg(reinterpret_cast<const double2*>(p));
     v[0] = a.x; v[1] = a.y;
   }
+  __device__ __forceinline__ void load(const double* __restrict__ p, uint64_t) { load(p); }
   __device__ __forceinline__ void zero() { v[0] = v[1] = 0.0; }
 };
 

@@ -46,6 +46,9 @@ template <typename T> struct DrawParams {
   const int32_t* words;     // LDA [n_tokens]
   const int32_t* token_doc; // LDA [n_tokens]
   const int32_t* last_key;  // LDA master rule [n_docs]
+  const int32_t* token_pos; // LDA, optional: the token list is a permutation (vocabulary
+                            // tiles); token j is word token_pos[j] of doc token_doc[j] and its
+                            // original CSR index offsets[doc] + pos indexes z / units / stops
   int64_t n_tokens;         // LDA tokens / ROWS rows
   int64_t doc_base;         // LDA global doc id of local doc 0 / ROWS row_base
   int stop_mode;
@@ -58,6 +61,9 @@ template <typename T> struct DrawParams {
   int32_t* word_topic;
   int32_t* doc_topic;
   unsigned long long* err;  // [0] AllZero key (min), [1] stop range flag
+  int l2_policy_x;          // L2 policy of the phi / weights loads (see make_l2_policy)
+  int l2_policy_t;          // L2 policy of the theta loads
+  uint32_t opaque_zero;     // always 0; the compiler cannot prove it (see BlockRegs::join)
 };
 
 // Identity of the token/row a lane owns: global doc id (or row id), its hash
@@ -65,17 +71,19 @@ template <typename T> struct DrawParams {
 template <typename T, int MODE>
 __device__ __forceinline__ void token_keys(const DrawParams<T>& p, int64_t tok, int32_t doc, int W,
                                            uint64_t& ka, uint64_t& kb, unsigned long long& ekey,
-                                           int& r) {
+                                           int& r, int64_t& zidx) {
   if (MODE == MODE_ROWS) {
     int64_t id = p.doc_base + tok;
     ka = (uint64_t)id;
     kb = 0;
     ekey = (unsigned long long)id;
     r = (int)(((id % W) + W) % W);
+    zidx = tok;
   } else {
     int64_t gm = p.doc_base + doc;
     int64_t o0 = p.offsets[doc];
-    int64_t i = tok - o0;
+    int64_t i = p.token_pos ? (int64_t)p.token_pos[tok] : tok - o0;
+    zidx = o0 + i;
     int64_t key = i;
     if (p.key_rule == WD_KEYS_MASTER) {
       int64_t n = p.offsets[doc + 1] - o0;
@@ -118,50 +126,124 @@ __device__ __forceinline__ T make_stop(const DrawParams<T>& p, int64_t tok, T to
 }
 
 // ============================================================== butterfly
-template <typename T, int W, bool VEC, int MODE, bool UNI>
-__device__ __forceinline__ T bfly_blocks(const DrawParams<T>& p, const T* const (&prow)[Geo<W>::L],
-                                         const T* const (&trow)[Geo<W>::L],
-                                         const bool (&rvalid)[Geo<W>::L], int nb, int rem, int s,
-                                         T acc, T* __restrict__ S, int lane) {
-  using G = Geo<W>;
-  constexpr int E = G::E, L = G::L;
-  for (int b = 0; b < nb; ++b) {
-    const int64_t off = (int64_t)rem + (int64_t)b * W;
+__device__ __forceinline__ uint32_t lo_bits(float v) { return __float_as_uint(v); }
+__device__ __forceinline__ uint32_t lo_bits(double v) { return (uint32_t)__double_as_longlong(v); }
+__device__ __forceinline__ void or_bits(float& v, uint32_t d) { v = __uint_as_float(__float_as_uint(v) | d); }
+__device__ __forceinline__ void or_bits(double& v, uint32_t d) {
+  v = __longlong_as_double(__double_as_longlong(v) | (long long)d);
+}
+
+// One W-topic block of the 32-row chunk held in registers: L vector segments
+// of phi (or weights) per lane, plus theta (L segments, or one when every
+// row of the chunk belongs to the same document: UNI).
+template <typename T, int W, bool VEC, int MODE, bool UNI> struct BlockRegs {
+  static constexpr int E = Geo<W>::E, L = Geo<W>::L;
+  static constexpr int NT = MODE == MODE_LDA ? (UNI ? 1 : L) : 1;
+  Seg<T, E, VEC> x[L];
+  Seg<T, E, VEC> th[NT];
+  // every load is unconditional (invalid rows point at a valid row) so all
+  // of them are in flight before the first use
+  __device__ __forceinline__ void load(const T* const (&prow)[L], const T* const (&trow)[L], int64_t off,
+                                       uint64_t pol_x, uint64_t pol_t) {
+#pragma unroll
+    for (int kk = 0; kk < L; ++kk) x[kk].load(prow[kk] + off, pol_x);
+    if (MODE == MODE_LDA) {
+#pragma unroll
+      for (int i = 0; i < NT; ++i) th[i].load(trow[i] + off, pol_t);
+    }
+  }
+  // Make every consumer depend on EVERY load of the block (through an
+  // opaque runtime zero), so ptxas cannot interleave consumers between the
+  // loads to save registers: all of the block's loads stay in flight together.
+  __device__ __forceinline__ void join(uint32_t opaque_zero) {
+    uint32_t d = 0;
+#pragma unroll
+    for (int kk = 0; kk < L; ++kk) d ^= lo_bits(x[kk].v[0]);
+    if (MODE == MODE_LDA) {
+#pragma unroll
+      for (int i = 0; i < NT; ++i) d ^= lo_bits(th[i].v[0]);
+    }
+    d &= opaque_zero;
+#pragma unroll
+    for (int kk = 0; kk < L; ++kk) or_bits(x[kk].v[0], d);
+    if (MODE == MODE_LDA) {
+#pragma unroll
+      for (int i = 0; i < NT; ++i) or_bits(th[i].v[0], d);
+    }
+  }
+  // block total of this lane's own row: first log2(E) tree levels in
+  // registers, remaining log2(L) by the shuffle transpose-reduce
+  __device__ __forceinline__ T reduce(const bool (&rvalid)[L], int s) const {
     T q[L];
-    Seg<T, E, VEC> th_u;
-    if (MODE == MODE_LDA && UNI) th_u.load(trow[0] + off);
 #pragma unroll
     for (int kk = 0; kk < L; ++kk) {
-      Seg<T, E, VEC> x;
-      if (rvalid[kk]) x.load(prow[kk] + off); else x.zero();
       T a[E];
-      if (MODE == MODE_LDA) {
-        Seg<T, E, VEC> th;
-        if (UNI) th = th_u;
-        else if (rvalid[kk]) th.load(trow[kk] + off);
-        else th.zero();
 #pragma unroll
-        for (int e = 0; e < E; ++e) a[e] = mul_rn(th.v[e], x.v[e]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) a[e] = x.v[e];
-      }
-      q[kk] = Tree<T, E>::sum(a);  // first log2(E) butterfly levels, in registers
+      for (int e = 0; e < E; ++e)
+        a[e] = MODE == MODE_LDA ? mul_rn(th[UNI ? 0 : kk].v[e], x[kk].v[e]) : x[kk].v[e];
+      q[kk] = rvalid[kk] ? Tree<T, E>::sum(a) : T(0);
     }
-    // remaining log2(L) levels: transpose-reduce over lanes s ^ bit
 #pragma unroll
     for (int bit = 1, n = L; bit < L; bit <<= 1, n >>= 1) {
       const bool hi = (s & bit) != 0;
 #pragma unroll
       for (int t = 0; t < n / 2; ++t) {
-        T x0 = q[2 * t], x1 = q[2 * t + 1];
-        T send = hi ? x0 : x1;
-        T keep = hi ? x1 : x0;
+        const T x0 = q[2 * t], x1 = q[2 * t + 1];
+        const T send = hi ? x0 : x1;
+        const T keep = hi ? x1 : x0;
         q[t] = add_rn(keep, __shfl_xor_sync(FULL, send, bit));
       }
     }
-    acc = add_rn(acc, q[0]);  // sequential accumulation over blocks (kernels.py:221-223)
-    S[b * 32 + lane] = acc;
+    return q[0];
+  }
+};
+
+// Pass 1 over all blocks: running block sums S_b of the own row
+// (sequential over blocks, kernels.py:221-223).  Memory-level parallelism:
+//   PIPE = 1  one block's loads in flight, then its arithmetic;
+//   PIPE = 2  block b+1's loads issued before block b's arithmetic;
+//   PIPE = 3  two blocks' loads issued together, then both reduced.
+template <typename T, int W, bool VEC, int MODE, bool UNI, int PIPE>
+__device__ __forceinline__ T bfly_blocks(const T* const (&prow)[Geo<W>::L], const T* const (&trow)[Geo<W>::L],
+                                         const bool (&rvalid)[Geo<W>::L], int nb, int s, T acc,
+                                         T* __restrict__ S, int lane, uint64_t px, uint64_t pt,
+                                         uint32_t opaque_zero) {
+  using R = BlockRegs<T, W, VEC, MODE, UNI>;
+  if (PIPE == 1 || PIPE == 4) {
+    for (int b = 0; b < nb; ++b) {
+      R cur;
+      cur.load(prow, trow, (int64_t)b * W, px, pt);
+      if (PIPE == 4) cur.join(opaque_zero);
+      acc = add_rn(acc, cur.reduce(rvalid, s));
+      S[b * 32 + lane] = acc;
+    }
+  } else if (PIPE == 2) {
+    R cur;
+    if (nb > 0) cur.load(prow, trow, 0, px, pt);
+    for (int b = 0; b < nb; ++b) {
+      R nxt;
+      if (b + 1 < nb) nxt.load(prow, trow, (int64_t)(b + 1) * W, px, pt);
+      acc = add_rn(acc, cur.reduce(rvalid, s));
+      S[b * 32 + lane] = acc;
+      cur = nxt;
+    }
+  } else {
+    int b = 0;
+    for (; b + 1 < nb; b += 2) {
+      R c0, c1;
+      c0.load(prow, trow, (int64_t)b * W, px, pt);
+      c1.load(prow, trow, (int64_t)(b + 1) * W, px, pt);
+      acc = add_rn(acc, c0.reduce(rvalid, s));
+      S[b * 32 + lane] = acc;
+      acc = add_rn(acc, c1.reduce(rvalid, s));
+      S[(b + 1) * 32 + lane] = acc;
+    }
+    if (b < nb) {
+      R c0;
+      c0.load(prow, trow, (int64_t)b * W, px, pt);
+      acc = add_rn(acc, c0.reduce(rvalid, s));
+      S[b * 32 + lane] = acc;
+    }
   }
   return acc;
 }
@@ -186,7 +268,7 @@ template <typename T> struct Walk<T, 0> {
   static __device__ __forceinline__ void run(T*, T&, T&, T, int, int&) {}
 };
 
-template <typename T, int W, bool VEC, int MODE>
+template <typename T, int W, bool VEC, int MODE, int PIPE>
 __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
   using G = Geo<W>;
   constexpr int E = G::E, L = G::L, R = G::R;
@@ -202,6 +284,8 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
   const int64_t n = p.n_tokens;
   const int64_t n_chunks = (n + 31) >> 5;
   const int64_t wpb = blockDim.x >> 5;
+  const uint64_t pol_x = make_l2_policy(p.l2_policy_x);
+  const uint64_t pol_t = make_l2_policy(p.l2_policy_t);
   for (int64_t c = (int64_t)blockIdx.x * wpb + wib; c < n_chunks; c += (int64_t)gridDim.x * wpb) {
     const int64_t tok0 = c << 5;
     const bool my_valid = tok0 + lane < n;
@@ -218,12 +302,13 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
       const int k = kk * R + rg;
       rvalid[kk] = tok0 + k < n;
       if (MODE == MODE_LDA) {
+        // invalid rows read word 0 / doc 0 (valid memory); their sums are discarded
         const int32_t wk = __shfl_sync(FULL, my_word, k);
         const int32_t dk = __shfl_sync(FULL, my_doc, k);
-        prow[kk] = p.phi + (int64_t)wk * p.ld_phi + s * E;
-        trow[kk] = p.theta + (int64_t)dk * p.ld_theta + s * E;
+        prow[kk] = p.phi + (int64_t)wk * p.ld_phi + rem + s * E;
+        trow[kk] = p.theta + (int64_t)dk * p.ld_theta + rem + s * E;
       } else {
-        prow[kk] = p.phi + (tok0 + k) * p.ld_phi + s * E;
+        prow[kk] = p.phi + (rvalid[kk] ? tok0 + k : tok0) * p.ld_phi + rem + s * E;
         trow[kk] = nullptr;
       }
     }
@@ -248,8 +333,12 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
       const int32_t d0 = __shfl_sync(FULL, my_doc, 0);
       uni = __all_sync(FULL, !my_valid || my_doc == d0);
     }
-    if (uni) acc = bfly_blocks<T, W, VEC, MODE, true>(p, prow, trow, rvalid, nb, rem, s, acc, S, lane);
-    else acc = bfly_blocks<T, W, VEC, MODE, false>(p, prow, trow, rvalid, nb, rem, s, acc, S, lane);
+    if (uni)
+      acc = bfly_blocks<T, W, VEC, MODE, true, PIPE>(prow, trow, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
+                                                     p.opaque_zero);
+    else  // mixed-document LDA chunks carry L theta segments: no room to double-buffer
+      acc = bfly_blocks<T, W, VEC, MODE, false, (MODE == MODE_LDA && PIPE != 4 ? 1 : PIPE)>(
+          prow, trow, rvalid, nb, s, acc, S, lane, pol_x, pol_t, p.opaque_zero);
     __syncwarp();
     const T total = acc;
 
@@ -257,8 +346,9 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
       uint64_t ka, kb;
       unsigned long long ekey;
       int r;
-      token_keys<T, MODE>(p, own_tok, own_doc, W, ka, kb, ekey, r);
-      const T stop = make_stop<T>(p, own_tok, total, ka, kb, MODE == MODE_ROWS);
+      int64_t zidx;
+      token_keys<T, MODE>(p, own_tok, own_doc, W, ka, kb, ekey, r, zidx);
+      const T stop = make_stop<T>(p, zidx, total, ka, kb, MODE == MODE_ROWS);
       if (!(total > T(0))) atomicMin(p.err, ekey);
       // block bisection over S (kernels.py:337-346)
       int j = 0, k = nb - 1;
@@ -301,7 +391,7 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
           if (stop < a2) { result = t; break; }
         }
       }
-      p.z[own_tok] = result;
+      p.z[zidx] = result;
       if (MODE == MODE_LDA) {
         if (p.word_topic) atomicAdd(p.word_topic + (int64_t)own_word * K + result, 1);
         if (p.doc_topic) atomicAdd(p.doc_topic + (int64_t)own_doc * K + result, 1);
@@ -392,15 +482,16 @@ __global__ void __launch_bounds__(128) prefix_kernel(DrawParams<T> p, T* __restr
       uint64_t ka, kb;
       unsigned long long ekey;
       int r;
-      token_keys<T, MODE>(p, tok0 + lane, my_doc, WR, ka, kb, ekey, r);
-      const T stop = make_stop<T>(p, tok0 + lane, total, ka, kb, MODE == MODE_ROWS);
+      int64_t zidx;
+      token_keys<T, MODE>(p, tok0 + lane, my_doc, WR, ka, kb, ekey, r, zidx);
+      const T stop = make_stop<T>(p, zidx, total, ka, kb, MODE == MODE_ROWS);
       if (!(total > T(0))) atomicMin(p.err, ekey);
       int j = 0, k = K - 1;  // samp.py:65-77 bisection over the table
       while (j < k) {
         const int mid = (j + k) >> 1;
         if (stop < table[(int64_t)mid * stride + gl]) k = mid; else j = mid + 1;
       }
-      p.z[tok0 + lane] = j;
+      p.z[zidx] = j;
       if (MODE == MODE_LDA) {
         if (p.word_topic) atomicAdd(p.word_topic + (int64_t)my_word * K + j, 1);
         if (p.doc_topic) atomicAdd(p.doc_topic + (int64_t)my_doc * K + j, 1);

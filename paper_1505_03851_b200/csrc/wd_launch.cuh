@@ -4,7 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
+#include <type_traits>
 #include <mutex>
 #include <utility>
 
@@ -48,9 +50,27 @@ inline size_t prefix_smem() {
 }
 inline int64_t prefix_table_cols() { return (int64_t)device_sm_count() * kPrefixBlocksPerSM * kThreads; }
 
-template <typename T, int W, bool VEC, int MODE>
-int launch_bfly_inst(const DrawParams<T>& p, cudaStream_t st) {
-  const void* fn = (const void*)bfly_kernel<T, W, VEC, MODE>;
+// Block-loop variant (see bfly_blocks) per mode; WD_PIPE_ROWS / WD_PIPE_LDA
+// override the defaults for experiments.
+inline int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && e[0]) ? atoi(e) : dflt;
+}
+inline int pipe_variant(int mode) {
+  static int rows = env_int("WD_PIPE_ROWS", 2);
+  static int lda = env_int("WD_PIPE_LDA", 1);
+  return mode == MODE_ROWS ? rows : lda;
+}
+// L2 policies (0 normal, 1 evict_last, 2 evict_first); WD_L2_X / WD_L2_T override
+inline void l2_policies(int mode, int& px, int& pt) {
+  static int lx = env_int("WD_L2_X", -1), lt = env_int("WD_L2_T", -1);
+  px = lx >= 0 ? lx : (mode == MODE_LDA ? 0 : 0);
+  pt = lt >= 0 ? lt : 0;
+}
+
+template <typename T, int W, bool VEC, int MODE, int PIPE>
+int launch_bfly_pipe(const DrawParams<T>& p, cudaStream_t st) {
+  const void* fn = (const void*)bfly_kernel<T, W, VEC, MODE, PIPE>;
   const size_t per_warp = bfly_smem_per_warp<T>(W, p.K);
   int wpb = kThreads / 32;  // fewer warps per CTA when the block sums are large
   while (wpb > 1 && (size_t)wpb * per_warp > 227 * 1024) wpb >>= 1;
@@ -64,10 +84,24 @@ int launch_bfly_inst(const DrawParams<T>& p, cudaStream_t st) {
   int64_t cap = (int64_t)per_sm * device_sm_count();
   int grid = (int)(want < cap ? want : cap);
   if (grid <= 0) return WD_OK;
-  bfly_kernel<T, W, VEC, MODE><<<grid, threads, smem, st>>>(p);
+  bfly_kernel<T, W, VEC, MODE, PIPE><<<grid, threads, smem, st>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { set_last_cuda_error(e); return WD_ERR_CUDA; }
   return WD_OK;
+}
+
+template <typename T, int W, bool VEC, int MODE>
+int launch_bfly_inst(const DrawParams<T>& p0, cudaStream_t st) {
+  DrawParams<T> p = p0;
+  l2_policies(MODE, p.l2_policy_x, p.l2_policy_t);
+  // the multi-block variants are instantiated for the fp32 W=32 vector path only
+  if (std::is_same<T, float>::value && W == 32 && VEC) {
+    const int v = pipe_variant(MODE);
+    if (v == 2) return launch_bfly_pipe<T, W, VEC, MODE, 2>(p, st);
+    if (v == 3) return launch_bfly_pipe<T, W, VEC, MODE, 3>(p, st);
+    if (v == 4) return launch_bfly_pipe<T, W, VEC, MODE, 4>(p, st);
+  }
+  return launch_bfly_pipe<T, W, VEC, MODE, 1>(p, st);
 }
 
 template <typename T, bool VEC, int MODE>

@@ -50,12 +50,14 @@ __device__ __forceinline__ float u01(uint32_t x) { return ((float)(x >> 8) + 0.5
 
 // log of a Gamma(a, 1) variate (Marsaglia & Tsang 2000; a < 1 via the
 // boost Gamma(a) = Gamma(a + 1) * U^(1/a), the same construction numpy uses).
+// Transcendentals use the SFU approximations (__logf, __sinf, rsqrtf): this
+// path is statistical, not bitwise (this file is compiled with FMA allowed).
 __device__ float log_gamma_draw(float a, uint64_t seed, uint64_t row, uint32_t k) {
   uint32_t ctr = 0;
   Philox4 r = philox4(seed, row, k, ctr++);
   float boost = 0.f;
   if (a < 1.f) {
-    boost = logf(u01(r.w)) / a;
+    boost = __logf(u01(r.w)) * __frcp_rn(a);
     a += 1.f;
   }
   const float d = a - (1.f / 3.f);
@@ -63,19 +65,18 @@ __device__ float log_gamma_draw(float a, uint64_t seed, uint64_t row, uint32_t k
   for (int attempt = 0; attempt < 64; ++attempt) {
     if (attempt > 0) r = philox4(seed, row, k, ctr++);
     // Box-Muller normal from (x, y)
-    const float rad = sqrtf(-2.f * logf(u01(r.x)));
-    float s, co;
-    sincospif(2.f * u01(r.y), &s, &co);
-    const float x = rad * co;
+    const float m2l = -2.f * __logf(u01(r.x));
+    const float rad = m2l * rsqrtf(m2l);
+    const float x = rad * __cosf(6.28318530718f * (u01(r.y) - 0.5f));
     float v = 1.f + c * x;
     if (v <= 0.f) continue;
     v = v * v * v;
     const float u = u01(r.z);
     const float x2 = x * x;
-    if (u < 1.f - 0.0331f * x2 * x2 || logf(u) < 0.5f * x2 + d * (1.f - v + logf(v)))
-      return logf(d) + logf(v) + boost;
+    if (u < 1.f - 0.0331f * x2 * x2 || __logf(u) < 0.5f * x2 + d * (1.f - v + __logf(v)))
+      return __logf(d * v) + boost;
   }
-  return logf(d) + boost;  // unreachable in practice (acceptance > 95% per attempt)
+  return __logf(d) + boost;  // unreachable in practice (acceptance > 95% per attempt)
 }
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(256) theta_kernel(const int32_t* __restrict__ 
     mx = warp_max(mx);
     float sum = 0.f;
     for (int k = lane; k < K; k += 32) {
-      const float e = expf(lg[k] - mx);
+      const float e = __expf(lg[k] - mx);
       lg[k] = e;
       sum += e;
     }
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(kPhiThreads) phi_pass(int pass, const int32_t*
         *p = (T)lgv;
         acc = fmaxf(acc, lgv);
       } else if (pass == 1) {
-        const float e = expf((float)*p - cs);
+        const float e = __expf((float)*p - cs);
         *p = (T)e;
         acc += e;
       } else {

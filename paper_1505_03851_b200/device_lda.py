@@ -20,14 +20,18 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from .kernels import DeviceCorpus, SeededStops, draw_z_device, raise_for_err
+from .kernels import DeviceCorpus, SeededStops, combine_err, draw_z_device, raise_for_err
 from .rng import derive_seed
+
+# phi slice kept L2-resident per draw pass (126 MB L2; measured: 41 MB slices
+# run at the L2-resident rate, 82 MB ones do not -- profiles/)
+DEFAULT_VOCAB_TILE_BYTES = 40 << 20
 
 
 class DeviceLDA:
     def __init__(self, corpus: DeviceCorpus, n_topics: int, vocab_size: int, *, lanes: int = 32, dtype=None,
                  alpha: float = 0.1, beta: float = 0.01, seed: int = 0, kernel: str = "butterfly",
-                 process_group=None, theta=None, phi=None):
+                 process_group=None, theta=None, phi=None, vocab_tile_bytes: int | None = DEFAULT_VOCAB_TILE_BYTES):
         import torch
 
         _lib.require_cuda()
@@ -46,12 +50,18 @@ class DeviceLDA:
         self.phi = phi if phi is not None else torch.empty((self.V, self.K), dtype=self.dtype, device=dev)
         self.z = torch.zeros(corpus.n_tokens, dtype=torch.int32, device=dev)
         self.word_topic = torch.zeros((self.V, self.K), dtype=torch.int32, device=dev)
-        self.err = torch.empty(2, dtype=torch.int64, device=dev)
         L = _lib.load()
         self._phi_ws = torch.empty(int(L.wd_resample_phi_workspace_bytes(self.K)), dtype=torch.uint8, device=dev)
         self._ll_ws = torch.empty(8 * (corpus.n_docs + self.K) + 8, dtype=torch.uint8, device=dev)
         self._ll_out = torch.zeros(1, dtype=torch.float64, device=dev)
         self._dt = _lib.WD_FLOAT32 if self.dtype == torch.float32 else _lib.WD_FLOAT64
+        esz = 4 if self.dtype == torch.float32 else 8
+        self.tiles = None
+        if vocab_tile_bytes and self.V * self.K * esz > vocab_tile_bytes:
+            rows = max(1, int(vocab_tile_bytes // (self.K * esz)))
+            self.tiles = corpus.vocab_tiles(rows)
+        n_err = self.tiles.n_tiles if self.tiles is not None else 1
+        self.err = torch.empty((n_err, 2), dtype=torch.int64, device=dev)
 
     # ------------------------------------------------------------ init
     def init_uniform(self, low: float = 0.1, high: float = 1.0, seed: int | None = None):
@@ -79,7 +89,7 @@ class DeviceLDA:
         self.word_topic.zero_()
         draw_z_device(self.kernel, self.corpus, self.theta, self.phi, SeededStops(derive_seed(self.seed, 1, t)),
                       self.lanes, z=self.z, word_topic=self.word_topic if fused_counts else None, err=self.err,
-                      check=False)
+                      check=False, tiles=self.tiles)
 
     def allreduce_counts(self):
         if self.pg is not None:
@@ -102,7 +112,7 @@ class DeviceLDA:
         self.resample(t)
 
     def check_errors(self):
-        raise_for_err(self.err.cpu().numpy().view(np.uint64), _lib.WD_KEYS_MASTER, self.lanes)
+        raise_for_err(combine_err(self.err), _lib.WD_KEYS_MASTER, self.lanes)
 
     # -------------------------------------------------- log-likelihood
     def log_likelihood(self) -> float:

@@ -28,6 +28,8 @@ from .sampling import AllZeroError
 from .warp import Trace, WarpConfig
 
 __all__ = [
+    "VocabTiles",
+    "combine_err",
     "StopOutOfRangeError",
     "SeededStops",
     "InjectedStops",
@@ -179,6 +181,13 @@ class DeviceCorpus:
             raise ValueError("word lists shorter than the document lengths")
         return cls.from_csr(offsets, flat, doc_base, vocab_size)
 
+    def vocab_tiles(self, rows_per_tile: int) -> VocabTiles:
+        """Token list regrouped by vocabulary tile (cached per tile size)."""
+        key = ("tiles", int(rows_per_tile))
+        if key not in self._last_key:
+            self._last_key[key] = _build_vocab_tiles(self, int(rows_per_tile))
+        return self._last_key[key]
+
     def last_key(self, lanes: int):
         if lanes not in self._last_key:
             torch = _torch()
@@ -189,6 +198,43 @@ class DeviceCorpus:
                        "wd_corpus_prepare")
             self._last_key[lanes] = lk
         return self._last_key[lanes]
+
+
+@dataclass
+class VocabTiles:
+    """The corpus' tokens regrouped by vocabulary tile.
+
+    Tile t holds the tokens whose word lies in [t*rows, (t+1)*rows); inside a
+    tile the tokens keep CSR (document, position) order.  Drawing tile by tile
+    keeps the active slice of phi (rows x K) resident in the 126 MB L2 while
+    theta rows stream; z, units and the hash keys still use each token's
+    original (document, position), so results are bit-identical to the
+    untiled draw.
+    """
+
+    words: object
+    token_doc: object
+    token_pos: object
+    bounds: list
+    rows_per_tile: int
+
+    @property
+    def n_tiles(self) -> int:
+        return len(self.bounds) - 1
+
+
+def _build_vocab_tiles(corpus: "DeviceCorpus", rows_per_tile: int) -> VocabTiles:
+    torch = _torch()
+    tile = torch.div(corpus.words, rows_per_tile, rounding_mode="floor").to(torch.int32)
+    _, order = torch.sort(tile, stable=True)
+    words = corpus.words[order].contiguous()
+    doc = corpus.token_doc[order].contiguous()
+    pos = (order - corpus.offsets[doc.long()]).to(torch.int32).contiguous()
+    n_tiles = int(tile.max().item()) + 1 if corpus.n_tokens else 1
+    counts = torch.bincount(tile.long(), minlength=n_tiles).cpu().numpy()
+    bounds = [0] + np.cumsum(counts).tolist()
+    del order, tile
+    return VocabTiles(words, doc, pos, [int(b) for b in bounds], int(rows_per_tile))
 
 
 _DTYPES = {"float32": _lib.WD_FLOAT32, "float64": _lib.WD_FLOAT64}
@@ -278,13 +324,16 @@ def raise_for_err(err_host, key_rule: int, lanes: int):
 
 
 def draw_z_device(kernel: str, corpus: DeviceCorpus, theta, phi, stops, lanes: int = 32, *, z=None,
-                  word_topic=None, doc_topic=None, err=None, check: bool = True, stream=None):
+                  word_topic=None, doc_topic=None, err=None, check: bool = True, stream=None,
+                  tiles: VocabTiles | None = None):
     """Device-resident draw.  theta [n_docs, K], phi [V, K] CUDA tensors
     (float32 or float64, same dtype, row stride = leading dim).  Returns z
     (int32 CUDA tensor, CSR token order).  word_topic / doc_topic (int32) are
-    incremented in the same kernel when given.  check=False skips the host
-    synchronisation on the error word (err must then be supplied and
-    inspected by the caller, e.g. with raise_for_err)."""
+    incremented in the same kernel when given.  tiles (corpus.vocab_tiles)
+    draws tile by tile so each phi slice stays L2-resident; z is identical.
+    check=False skips the host synchronisation on the error word (err, shape
+    [n_launches, 2], must then be supplied and inspected by the caller with
+    raise_for_err(combine_err(err)))."""
     torch = _torch()
     if kernel not in _KERNEL_SPEC:
         raise ValueError(f"unknown kernel {kernel!r}; pick one of {sorted(_KERNEL_SPEC)}")
@@ -308,22 +357,39 @@ def draw_z_device(kernel: str, corpus: DeviceCorpus, theta, phi, stops, lanes: i
         raise ValueError("units do not cover every token")
     if z is None:
         z = torch.empty(corpus.n_tokens, dtype=torch.int32, device=dev)
-    own_err = err is None
-    if own_err:
-        err = torch.empty(2, dtype=torch.int64, device=dev)
+    if tiles is None:
+        launches = [(corpus.words, corpus.token_doc, None, 0, corpus.n_tokens)]
+    else:
+        launches = [(tiles.words, tiles.token_doc, tiles.token_pos, a, b - a)
+                    for a, b in zip(tiles.bounds[:-1], tiles.bounds[1:]) if b > a]
+    if err is None or err.numel() < 2 * max(1, len(launches)):
+        err = torch.empty((max(1, len(launches)), 2), dtype=torch.int64, device=dev)
+    err2 = err.view(-1, 2)
     last_key = corpus.last_key(lanes) if (mode == _lib.WD_STOPS_SEEDED and key_rule == _lib.WD_KEYS_MASTER) else None
     ws, ws_bytes = _workspace(variant, dt, lanes, K, dev)
     L = _lib.load()
-    _lib.check(
-        L.wd_draw_z(variant, dt, int(lanes), theta.data_ptr(), theta.stride(0), phi.data_ptr(), phi.stride(0), K,
-                    corpus.offsets.data_ptr(), corpus.words.data_ptr(), corpus.token_doc.data_ptr(),
-                    _lib.ptr(last_key), corpus.n_docs, corpus.n_tokens, corpus.doc_base, mode, key_rule,
-                    int(seed) & ((1 << 64) - 1), _lib.ptr(units), None, z.data_ptr(), _lib.ptr(word_topic),
-                    _lib.ptr(doc_topic), err.data_ptr(), _lib.ptr(ws), ws_bytes, _lib.stream_handle(stream)),
-        "wd_draw_z")
+    st = _lib.stream_handle(stream)
+    for li, (wds, tdoc, tpos, a, n) in enumerate(launches):
+        _lib.check(
+            L.wd_draw_z(variant, dt, int(lanes), theta.data_ptr(), theta.stride(0), phi.data_ptr(), phi.stride(0), K,
+                        corpus.offsets.data_ptr(), wds.data_ptr() + 4 * a, tdoc.data_ptr() + 4 * a,
+                        None if tpos is None else tpos.data_ptr() + 4 * a, _lib.ptr(last_key), corpus.n_docs, n,
+                        corpus.doc_base, mode, key_rule, int(seed) & ((1 << 64) - 1), _lib.ptr(units), None,
+                        z.data_ptr(), _lib.ptr(word_topic), _lib.ptr(doc_topic), err2[li].data_ptr(), _lib.ptr(ws),
+                        ws_bytes, st),
+            "wd_draw_z")
+    if not launches:
+        err2.zero_()
+        err2[:, 0] = -1
     if check:
-        raise_for_err(err.cpu().numpy().view(np.uint64), key_rule, lanes)
+        raise_for_err(combine_err(err2[: max(1, len(launches))]), key_rule, lanes)
     return z
+
+
+def combine_err(err) -> np.ndarray:
+    """Fold per-launch error words [n, 2] into one (min AllZero key, any range flag)."""
+    e = err.reshape(-1, 2).cpu().numpy().view(np.uint64)
+    return np.array([e[:, 0].min(), e[:, 1].max()], dtype=np.uint64)
 
 
 def _to_host_ragged(z_dev, N):

@@ -331,3 +331,31 @@ def test_full_size_rows_k1024_properties():
     seed6 = wd.derive_seed(2026, 6)
     exp = np.array([O.sample_rows(sub[j:j + 1], 32, seed6, row0=int(r))[0] for j, r in enumerate(rows)])
     np.testing.assert_array_equal(zbn[rows], exp)
+
+
+@pytest.mark.parametrize("kernel", ["butterfly", "transposed", "basic"])
+def test_vocab_tiled_draw_identical(kernel):
+    """Drawing tile by tile over the vocabulary (phi slices L2-resident) gives
+    the same z and counts as the untiled draw, for every kernel and stop mode."""
+    gen = np.random.default_rng(11)
+    M, V, K = 640, 1000, 128
+    N, off, words = _random_corpus(gen, M, V, 40)
+    theta = gen.uniform(0.05, 1, size=(M, K)).astype(np.float32)
+    phi = gen.uniform(0.05, 1, size=(V, K)).astype(np.float32)
+    dc = wd.DeviceCorpus.from_csr(off, words.astype(np.int32))
+    th, ph = _cuda(theta), _cuda(phi)
+    tiles = dc.vocab_tiles(137)
+    assert tiles.n_tiles == -(-V // 137) and tiles.bounds[-1] == dc.n_tokens
+    u = _cuda(gen.random(int(off[-1])))
+    for stops in (wd.SeededStops(5), u):
+        wt0 = torch.zeros((V, K), dtype=torch.int32, device="cuda")
+        wt1 = torch.zeros((V, K), dtype=torch.int32, device="cuda")
+        z0 = wd.draw_z_device(kernel, dc, th, ph, stops, 32, word_topic=wt0)
+        z1 = wd.draw_z_device(kernel, dc, th, ph, stops, 32, word_topic=wt1, tiles=tiles)
+        np.testing.assert_array_equal(z0.cpu().numpy(), z1.cpu().numpy())
+        np.testing.assert_array_equal(wt0.cpu().numpy(), wt1.cpu().numpy())
+    exp, _ = O.draw_z_csr(theta, phi, off, words, W=32, seed=5,
+                          variant=O.BUTTERFLY if kernel == "butterfly" else O.PREFIX,
+                          key_rule=O.KEY_POSITION if kernel == "basic" else O.KEY_MASTER)
+    z = wd.draw_z_device(kernel, dc, th, ph, wd.SeededStops(5), 32, tiles=tiles).cpu().numpy()
+    np.testing.assert_array_equal(z, exp)

@@ -40,7 +40,7 @@ def test_library_loads_and_exports_every_symbol():
 def test_invalid_arguments_rejected_without_gpu():
     L = _lib.load()
     # validation happens before any device work
-    assert L.wd_draw_z(0, 0, 3, None, 0, None, 0, 8, None, None, None, None, 0, 0, 0, 0, 0, 0, None, None,
+    assert L.wd_draw_z(0, 0, 3, None, 0, None, 0, 8, None, None, None, None, None, 0, 0, 0, 0, 0, 0, None, None,
                        None, None, None, None, None, 0, None) == 1  # lanes=3
     assert L.wd_units(0, 3, None, None, 1, None, None) == 1
     assert L.wd_sample_rows(0, 2, 32, None, 0, 1, 8, 0, 0, 0, None, None, None, None, None, 0, None) == 1

@@ -1,0 +1,82 @@
+"""World-size-2 (gloo, CPU) coverage of the N>1 path: 32-aligned token-balanced
+document shards, global doc ids, per-rank draws and the word-topic all-reduce
+must reproduce the single-process result exactly.  The per-rank draw here is
+the CPU oracle (the device kernel is checked against the same oracle and the
+same doc_base semantics in tests/test_gpu_parity.py)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1505_03851_b200.sharding import shard_csr, shard_ranges
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _problem(seed=3):
+    gen = np.random.default_rng(seed)
+    M, V, K = 256, 120, 48
+    N = np.maximum(gen.poisson(15, size=M), 0)
+    N[::17] = 0
+    off = np.concatenate([[0], np.cumsum(N)]).astype(np.int64)
+    words = gen.integers(0, V, size=int(off[-1])).astype(np.int64)
+    theta = gen.uniform(0.05, 1, size=(M, K)).astype(np.float32)
+    phi = gen.uniform(0.05, 1, size=(V, K)).astype(np.float32)
+    return M, V, K, N, off, words, theta, phi
+
+
+def _worker(rank, world, port, out_dir):
+    from oracle import oracle as O
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    M, V, K, N, off, words, theta, phi = _problem()
+    lo, hi = shard_ranges(N, world)[rank]
+    soff, swords = shard_csr(off, words, lo, hi)
+    seed = O.derive_seed(7, 1, 0)
+    z, err = O.draw_z_csr(theta[lo:hi], phi, soff, swords, W=32, seed=seed, doc_base=lo)
+    assert err is None
+    _, wt = O.topic_counts(soff, swords, z, K, V)
+    wt_t = torch.from_numpy(wt.astype(np.int32))
+    dist.all_reduce(wt_t)
+    np.save(os.path.join(out_dir, f"z{rank}.npy"), z)
+    np.save(os.path.join(out_dir, f"wt{rank}.npy"), wt_t.numpy())
+    dist.destroy_process_group()
+
+
+def test_shard_ranges_aligned_and_balanced():
+    gen = np.random.default_rng(0)
+    N = gen.poisson(200, size=32 * 1000)
+    for world in (1, 2, 3, 4, 8):
+        r = shard_ranges(N, world)
+        assert r[0][0] == 0 and r[-1][1] == N.size
+        assert all(a % 32 == 0 and b % 32 == 0 and a <= b for a, b in r)
+        assert all(r[i][1] == r[i + 1][0] for i in range(world - 1))
+        tok = [int(N[a:b].sum()) for a, b in r]
+        assert max(tok) - min(tok) <= 2 * int(N.reshape(-1, 32).sum(1).max())
+    with pytest.raises(ValueError):
+        shard_ranges(np.ones(33), 2)
+
+
+def test_two_rank_gloo_matches_single_process(tmp_path):
+    from oracle import oracle as O
+
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    M, V, K, N, off, words, theta, phi = _problem()
+    z_full, err = O.draw_z_csr(theta, phi, off, words, W=32, seed=O.derive_seed(7, 1, 0))
+    _, wt_full = O.topic_counts(off, words, z_full, K, V)
+    z_parts = np.concatenate([np.load(tmp_path / f"z{r}.npy") for r in range(world)])
+    np.testing.assert_array_equal(z_parts, z_full)
+    for r in range(world):
+        np.testing.assert_array_equal(np.load(tmp_path / f"wt{r}.npy"), wt_full)

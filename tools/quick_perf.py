@@ -25,9 +25,10 @@ def t_events(fn, iters=10, warm=3):
 
 def main():
     res = {}
-    n = 1 << 20
+    what = sys.argv[2] if len(sys.argv) > 2 else "both"
+    n = 1 << 20 if what != "lda" else 0
     g = torch.Generator(device="cuda").manual_seed(0)
-    for K in [int(k) for k in (sys.argv[1] if len(sys.argv) > 1 else "32,64,128,256,512,1024,2048").split(",")]:
+    for K in [int(k) for k in (sys.argv[1] if len(sys.argv) > 1 else "32,64,128,256,512,1024,2048").split(",")] if n else []:
         w = torch.rand((n, K), generator=g, device="cuda") * 0.9 + 0.1
         out = torch.empty(n, dtype=torch.int32, device="cuda")
         err = torch.empty(2, dtype=torch.int64, device="cuda")
@@ -39,6 +40,8 @@ def main():
         res[f"rows_K{K}"] = row
         print(K, json.dumps(row), flush=True)
         del w
+    if what == "rows":
+        return
     # LDA draw, cfg4-like but 200k docs
     M, V, K = 200_000, 40_000, 1024
     lengths = torch.poisson(torch.full((M,), 200.0, device="cuda"), generator=g).clamp_(min=1).long()
@@ -52,7 +55,7 @@ def main():
     z = torch.empty(T, dtype=torch.int32, device="cuda")
     err = torch.empty(2, dtype=torch.int64, device="cuda")
     wt = torch.zeros((V, K), dtype=torch.int32, device="cuda")
-    for kern in ("butterfly", "transposed"):
+    for kern in ("butterfly",):
         dt = t_events(lambda: wd.draw_z_device(kern, dc, theta, phi, wd.SeededStops(3), 32, z=z, err=err,
                                                check=False), iters=5, warm=2)
         nb = T * (4 * K + 4 * K * M / T + 8)
