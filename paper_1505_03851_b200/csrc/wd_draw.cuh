@@ -134,16 +134,18 @@ __device__ __forceinline__ void or_bits(double& v, uint32_t d) {
 }
 
 // One W-topic block of the 32-row chunk held in registers: L vector segments
-// of phi (or weights) per lane, plus theta (L segments, or one when every
-// row of the chunk belongs to the same document: UNI).
-template <typename T, int W, bool VEC, int MODE, bool UNI> struct BlockRegs {
+// of phi (or weights) per lane, plus theta segments: ND = 1 when every row of
+// the chunk belongs to one document, ND = 2 when to two (rows pick theirs by
+// the bit mask dsel), ND = 0 one theta segment per row.
+template <typename T, int W, bool VEC, int MODE, int ND> struct BlockRegs {
   static constexpr int E = Geo<W>::E, L = Geo<W>::L;
-  static constexpr int NT = MODE == MODE_LDA ? (UNI ? 1 : L) : 1;
+  static constexpr int NT = MODE == MODE_LDA ? (ND == 0 ? L : ND) : 1;
+  static constexpr int LT = L < 2 ? 2 : L;  // theta pointer slots (>= 2 for ND == 2)
   Seg<T, E, VEC> x[L];
   Seg<T, E, VEC> th[NT];
   // every load is unconditional (invalid rows point at a valid row) so all
   // of them are in flight before the first use
-  __device__ __forceinline__ void load(const T* const (&prow)[L], const T* const (&trow)[L], int64_t off,
+  __device__ __forceinline__ void load(const T* const (&prow)[L], const T* const (&trow)[LT], int64_t off,
                                        uint64_t pol_x, uint64_t pol_t) {
 #pragma unroll
     for (int kk = 0; kk < L; ++kk) x[kk].load(prow[kk] + off, pol_x);
@@ -173,14 +175,21 @@ template <typename T, int W, bool VEC, int MODE, bool UNI> struct BlockRegs {
   }
   // block total of this lane's own row: first log2(E) tree levels in
   // registers, remaining log2(L) by the shuffle transpose-reduce
-  __device__ __forceinline__ T reduce(const bool (&rvalid)[L], int s) const {
+  __device__ __forceinline__ T reduce(const bool (&rvalid)[L], int s, uint32_t dsel) const {
     T q[L];
 #pragma unroll
     for (int kk = 0; kk < L; ++kk) {
       T a[E];
 #pragma unroll
-      for (int e = 0; e < E; ++e)
-        a[e] = MODE == MODE_LDA ? mul_rn(th[UNI ? 0 : kk].v[e], x[kk].v[e]) : x[kk].v[e];
+      for (int e = 0; e < E; ++e) {
+        T t = T(0);
+        if (MODE == MODE_LDA) {
+          if (ND == 1) t = th[0].v[e];
+          else if (ND == 2) t = ((dsel >> kk) & 1u) ? th[NT - 1].v[e] : th[0].v[e];
+          else t = th[kk].v[e];
+        }
+        a[e] = MODE == MODE_LDA ? mul_rn(t, x[kk].v[e]) : x[kk].v[e];
+      }
       q[kk] = rvalid[kk] ? Tree<T, E>::sum(a) : T(0);
     }
 #pragma unroll
@@ -203,18 +212,19 @@ template <typename T, int W, bool VEC, int MODE, bool UNI> struct BlockRegs {
 //   PIPE = 1  one block's loads in flight, then its arithmetic;
 //   PIPE = 2  block b+1's loads issued before block b's arithmetic;
 //   PIPE = 3  two blocks' loads issued together, then both reduced.
-template <typename T, int W, bool VEC, int MODE, bool UNI, int PIPE>
-__device__ __forceinline__ T bfly_blocks(const T* const (&prow)[Geo<W>::L], const T* const (&trow)[Geo<W>::L],
+template <typename T, int W, bool VEC, int MODE, int ND, int PIPE>
+__device__ __forceinline__ T bfly_blocks(const T* const (&prow)[Geo<W>::L],
+                                         const T* const (&trow)[(Geo<W>::L < 2 ? 2 : Geo<W>::L)],
                                          const bool (&rvalid)[Geo<W>::L], int nb, int s, T acc,
                                          T* __restrict__ S, int lane, uint64_t px, uint64_t pt,
-                                         uint32_t opaque_zero) {
-  using R = BlockRegs<T, W, VEC, MODE, UNI>;
+                                         uint32_t opaque_zero, uint32_t dsel) {
+  using R = BlockRegs<T, W, VEC, MODE, ND>;
   if (PIPE == 1 || PIPE == 4) {
     for (int b = 0; b < nb; ++b) {
       R cur;
       cur.load(prow, trow, (int64_t)b * W, px, pt);
       if (PIPE == 4) cur.join(opaque_zero);
-      acc = add_rn(acc, cur.reduce(rvalid, s));
+      acc = add_rn(acc, cur.reduce(rvalid, s, dsel));
       S[b * 32 + lane] = acc;
     }
   } else if (PIPE == 2) {
@@ -223,7 +233,7 @@ __device__ __forceinline__ T bfly_blocks(const T* const (&prow)[Geo<W>::L], cons
     for (int b = 0; b < nb; ++b) {
       R nxt;
       if (b + 1 < nb) nxt.load(prow, trow, (int64_t)(b + 1) * W, px, pt);
-      acc = add_rn(acc, cur.reduce(rvalid, s));
+      acc = add_rn(acc, cur.reduce(rvalid, s, dsel));
       S[b * 32 + lane] = acc;
       cur = nxt;
     }
@@ -233,15 +243,15 @@ __device__ __forceinline__ T bfly_blocks(const T* const (&prow)[Geo<W>::L], cons
       R c0, c1;
       c0.load(prow, trow, (int64_t)b * W, px, pt);
       c1.load(prow, trow, (int64_t)(b + 1) * W, px, pt);
-      acc = add_rn(acc, c0.reduce(rvalid, s));
+      acc = add_rn(acc, c0.reduce(rvalid, s, dsel));
       S[b * 32 + lane] = acc;
-      acc = add_rn(acc, c1.reduce(rvalid, s));
+      acc = add_rn(acc, c1.reduce(rvalid, s, dsel));
       S[(b + 1) * 32 + lane] = acc;
     }
     if (b < nb) {
       R c0;
       c0.load(prow, trow, (int64_t)b * W, px, pt);
-      acc = add_rn(acc, c0.reduce(rvalid, s));
+      acc = add_rn(acc, c0.reduce(rvalid, s, dsel));
       S[b * 32 + lane] = acc;
     }
   }
@@ -328,17 +338,42 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
       }
     }
     const T prem = acc;
-    bool uni = false;
+    // theta rows the chunk needs: one document (ND=1), two (ND=2: the rows of
+    // the second one are flagged in dsel), or more (ND=0: per-row loads).
+    // Chunks are CSR-ordered, so their documents are nondecreasing.
+    int nd = 1;
+    uint32_t dsel = 0;
+    const T* trow_nd[L < 2 ? 2 : L];
+#pragma unroll
+    for (int kk = 0; kk < L; ++kk) trow_nd[kk] = trow[kk];
+    if (L < 2) trow_nd[L < 2 ? 1 : 0] = trow[0];
     if (MODE == MODE_LDA) {
       const int32_t d0 = __shfl_sync(FULL, my_doc, 0);
-      uni = __all_sync(FULL, !my_valid || my_doc == d0);
+      const int32_t d1 = __reduce_max_sync(FULL, my_valid ? my_doc : d0);
+      if (d1 != d0) {
+        nd = __all_sync(FULL, !my_valid || my_doc == d0 || my_doc == d1) ? 2 : 0;
+        if (nd == 2) {
+#pragma unroll
+          for (int kk = 0; kk < L; ++kk) {
+            const int32_t dk = __shfl_sync(FULL, my_doc, kk * R + rg);
+            if (dk == d1 && rvalid[kk]) dsel |= 1u << kk;
+          }
+          trow_nd[0] = p.theta + (int64_t)d0 * p.ld_theta + rem + s * E;
+          trow_nd[1] = p.theta + (int64_t)d1 * p.ld_theta + rem + s * E;
+        }
+      } else {
+        trow_nd[0] = p.theta + (int64_t)d0 * p.ld_theta + rem + s * E;
+      }
     }
-    if (uni)
-      acc = bfly_blocks<T, W, VEC, MODE, true, PIPE>(prow, trow, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
-                                                     p.opaque_zero);
-    else  // mixed-document LDA chunks carry L theta segments: no room to double-buffer
-      acc = bfly_blocks<T, W, VEC, MODE, false, (MODE == MODE_LDA && PIPE != 4 ? 1 : PIPE)>(
-          prow, trow, rvalid, nb, s, acc, S, lane, pol_x, pol_t, p.opaque_zero);
+    if (nd == 1)
+      acc = bfly_blocks<T, W, VEC, MODE, 1, PIPE>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
+                                                  p.opaque_zero, 0u);
+    else if (MODE == MODE_LDA && nd == 2)
+      acc = bfly_blocks<T, W, VEC, MODE, 2, PIPE>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
+                                                  p.opaque_zero, dsel);
+    else  // >2 documents: L theta segments per block, no room to double-buffer
+      acc = bfly_blocks<T, W, VEC, MODE, 0, (MODE == MODE_LDA && PIPE != 4 ? 1 : PIPE)>(
+          prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t, p.opaque_zero, 0u);
     __syncwarp();
     const T total = acc;
 

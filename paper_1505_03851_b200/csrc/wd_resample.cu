@@ -48,13 +48,15 @@ __device__ __forceinline__ Philox4 philox4(uint64_t seed, uint64_t row, uint32_t
 // uniform in (0, 1): 24-bit mantissa, never 0
 __device__ __forceinline__ float u01(uint32_t x) { return ((float)(x >> 8) + 0.5f) * 0x1p-24f; }
 
-// log of a Gamma(a, 1) variate (Marsaglia & Tsang 2000; a < 1 via the
-// boost Gamma(a) = Gamma(a + 1) * U^(1/a), the same construction numpy uses).
-// Transcendentals use the SFU approximations (__logf, __sinf, rsqrtf): this
-// path is statistical, not bitwise (this file is compiled with FMA allowed).
-__device__ float log_gamma_draw(float a, uint64_t seed, uint64_t row, uint32_t k) {
-  uint32_t ctr = 0;
-  Philox4 r = philox4(seed, row, k, ctr++);
+// One Marsaglia-Tsang attempt (2000) for log Gamma(a, 1) from Philox block
+// (seed, row, topic, ctr); shapes a < 1 use the boost Gamma(a) = Gamma(a + 1)
+// * U^(1/a) (numpy's construction) with U taken from the same block -- its
+// acceptance depends only on the other three words, so U stays independent.
+// Evaluated in LOG space so alpha = 0.1 / beta = 0.01 shapes never underflow.
+// SFU approximations (__logf, __cosf, rsqrtf): statistical, not bitwise.
+__device__ __forceinline__ bool log_gamma_attempt(float a, uint64_t seed, uint64_t row, uint32_t k, uint32_t ctr,
+                                                  float& out) {
+  const Philox4 r = philox4(seed, row, k, ctr);
   float boost = 0.f;
   if (a < 1.f) {
     boost = __logf(u01(r.w)) * __frcp_rn(a);
@@ -62,21 +64,18 @@ __device__ float log_gamma_draw(float a, uint64_t seed, uint64_t row, uint32_t k
   }
   const float d = a - (1.f / 3.f);
   const float c = rsqrtf(9.f * d);
-  for (int attempt = 0; attempt < 64; ++attempt) {
-    if (attempt > 0) r = philox4(seed, row, k, ctr++);
-    // Box-Muller normal from (x, y)
-    const float m2l = -2.f * __logf(u01(r.x));
-    const float rad = m2l * rsqrtf(m2l);
-    const float x = rad * __cosf(6.28318530718f * (u01(r.y) - 0.5f));
-    float v = 1.f + c * x;
-    if (v <= 0.f) continue;
-    v = v * v * v;
-    const float u = u01(r.z);
-    const float x2 = x * x;
-    if (u < 1.f - 0.0331f * x2 * x2 || __logf(u) < 0.5f * x2 + d * (1.f - v + __logf(v)))
-      return __logf(d * v) + boost;
+  const float m2l = -2.f * __logf(u01(r.x));  // Box-Muller normal from (x, y)
+  const float x = m2l * rsqrtf(m2l) * __cosf(6.28318530718f * (u01(r.y) - 0.5f));
+  float v = 1.f + c * x;
+  if (v <= 0.f) return false;
+  v = v * v * v;
+  const float u = u01(r.z);
+  const float x2 = x * x;
+  if (u < 1.f - 0.0331f * x2 * x2 || __logf(u) < 0.5f * x2 + d * (1.f - v + __logf(v))) {
+    out = __logf(d * v) + boost;
+    return true;
   }
-  return __logf(d) + boost;  // unreachable in practice (acceptance > 95% per attempt)
+  return false;
 }
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -115,10 +114,19 @@ __global__ void __launch_bounds__(256) theta_kernel(const int32_t* __restrict__ 
     __syncwarp();
     const uint64_t row = (uint64_t)(doc_base + m);
     float mx = -INFINITY;
-    for (int k = lane; k < K; k += 32) {
-      const float v = log_gamma_draw(alpha + (float)hist[k], seed, row, (uint32_t)k);
-      lg[k] = v;
-      mx = fmaxf(mx, v);
+    // per-lane progress: a rejection costs that lane one more attempt instead
+    // of stalling the whole warp at every topic (divergence only at the tail)
+    uint32_t ctr = 0;
+    for (int k = lane; k < K;) {
+      float v;
+      if (log_gamma_attempt(alpha + (float)hist[k], seed, row, (uint32_t)k, ctr, v)) {
+        lg[k] = v;
+        mx = fmaxf(mx, v);
+        k += 32;
+        ctr = 0;
+      } else {
+        ++ctr;
+      }
     }
     mx = warp_max(mx);
     float sum = 0.f;
@@ -150,13 +158,23 @@ __global__ void __launch_bounds__(kPhiThreads) phi_pass(int pass, const int32_t*
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     float acc = pass == 0 ? -INFINITY : 0.f;
     const float cs = pass == 0 ? 0.f : colstat[k];
-    for (int64_t v = v0; v < v1; ++v) {
+    if (pass == 0) {
+      uint32_t ctr = 0;
+      for (int64_t v = v0; v < v1;) {
+        float lgv;
+        if (log_gamma_attempt(beta + (float)wt[v * (int64_t)K + k], seed, (uint64_t)v, (uint32_t)k, ctr, lgv)) {
+          phi[v * ld + k] = (T)lgv;
+          acc = fmaxf(acc, lgv);
+          ++v;
+          ctr = 0;
+        } else {
+          ++ctr;
+        }
+      }
+    }
+    for (int64_t v = v0; v < v1 && pass > 0; ++v) {
       T* p = phi + v * ld + k;
-      if (pass == 0) {
-        const float lgv = log_gamma_draw(beta + (float)wt[v * (int64_t)K + k], seed, (uint64_t)v, (uint32_t)k);
-        *p = (T)lgv;
-        acc = fmaxf(acc, lgv);
-      } else if (pass == 1) {
+      if (pass == 1) {
         const float e = __expf((float)*p - cs);
         *p = (T)e;
         acc += e;
