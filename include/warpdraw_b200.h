@@ -23,8 +23,8 @@
  *                  WD_KEYS_MASTER   : (doc/lanes) << 40 | word << 8 | doc%lanes
  *                  WD_KEYS_POSITION : doc << 32 | word
  *                  rows             : row id
- *       err[1] = 1 if an explicit stop was out of range (StopOutOfRangeError,
- *                kernels.py:329-331), else 0.
+ *       err[1] = 0 if an explicit stop was out of range (StopOutOfRangeError,
+ *                kernels.py:329-331), else UINT64_MAX.
  *     The library resets err at the start of each call.
  *
  * Arithmetic: IEEE binary32 / binary64, round-to-nearest, no FMA contraction,

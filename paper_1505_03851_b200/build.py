@@ -22,7 +22,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 OUT_DIR = os.path.join(PKG, "_lib")
-LIB = os.path.join(OUT_DIR, "libwarpdraw_b200.so")
+LIB = os.environ.get("WD_LIB_OUT") or os.path.join(OUT_DIR, "libwarpdraw_b200.so")
 SOURCES = ["wd_draw_f32.cu", "wd_draw_f64.cu", "wd_capi.cu", "wd_resample.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # sources whose results are statistical (device resample, log-likelihood)
@@ -41,6 +41,7 @@ def _flags(ptxas_verbose: bool):
          f"-I{INCLUDE}", f"-I{CSRC}", "--expt-relaxed-constexpr"]
     if ptxas_verbose:
         f += ["-Xptxas", "-v"]
+    f += os.environ.get("WD_EXTRA_FLAGS", "").split()  # experiments only
     return f
 
 
@@ -59,7 +60,7 @@ def build(force: bool = False, ptxas_verbose: bool = False, verbose: bool = True
     if not force and up_to_date():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
-    obj_dir = os.path.join(OUT_DIR, "obj")
+    obj_dir = os.path.join(os.path.dirname(LIB), "obj_" + os.path.basename(LIB).replace(".so", ""))
     os.makedirs(obj_dir, exist_ok=True)
     cc = nvcc()
     flags = _flags(ptxas_verbose)

@@ -115,6 +115,10 @@ static bool vec_ok(const void* ptr, int64_t ld, int K, int Weff, size_t esz) {
 template <typename T>
 static int draw_common(int variant, int lanes, int mode, DrawParams<T>& p, void* ws, size_t ws_bytes,
                        cudaStream_t st) {
+  // rows are addressed as 32-bit row index x 32-bit byte stride (RowSet)
+  if ((uint64_t)p.ld_phi * sizeof(T) >= (1ull << 32) || (uint64_t)p.ld_theta * sizeof(T) >= (1ull << 32) ||
+      (mode == MODE_ROWS && (uint64_t)p.n_tokens >= (1ull << 32)))
+    return WD_ERR_UNSUPPORTED;
   const int Weff = variant == WD_BUTTERFLY ? lanes : 32;
   const bool vec = vec_ok(p.phi, p.ld_phi, p.K, Weff, sizeof(T)) &&
                    (mode == MODE_ROWS || vec_ok(p.theta, p.ld_theta, p.K, Weff, sizeof(T)));
@@ -123,9 +127,8 @@ static int draw_common(int variant, int lanes, int mode, DrawParams<T>& p, void*
 
 static int reset_err(uint64_t* err, cudaStream_t st) {
   if (err == nullptr) return WD_ERR_INVALID_ARGUMENT;
-  if (cudaMemsetAsync(err, 0xFF, sizeof(uint64_t), st) != cudaSuccess ||
-      cudaMemsetAsync(err + 1, 0, sizeof(uint64_t), st) != cudaSuccess)
-    return check_launch();
+  // both words start at all-ones: one memset (one launch) per call
+  if (cudaMemsetAsync(err, 0xFF, 2 * sizeof(uint64_t), st) != cudaSuccess) return check_launch();
   return WD_OK;
 }
 

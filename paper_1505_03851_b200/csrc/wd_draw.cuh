@@ -36,6 +36,12 @@ namespace wd {
 
 enum { MODE_LDA = 0, MODE_ROWS = 1 };
 
+// Minimum resident CTAs per SM requested for the LDA draw (caps registers so
+// that enough warps are resident to cover L2 gather latency).
+#ifndef WD_LDA_MIN_BLOCKS
+#define WD_LDA_MIN_BLOCKS 6
+#endif
+
 template <typename T> struct DrawParams {
   const T* theta;  // LDA: doc rows (ld_theta); ROWS: unused
   int64_t ld_theta;
@@ -60,7 +66,7 @@ template <typename T> struct DrawParams {
   int32_t* z;
   int32_t* word_topic;
   int32_t* doc_topic;
-  unsigned long long* err;  // [0] AllZero key (min), [1] stop range flag
+  unsigned long long* err;  // [0] AllZero key (min), [1] stop range flag (0 = bad)
   int l2_policy_x;          // L2 policy of the phi / weights loads (see make_l2_policy)
   int l2_policy_t;          // L2 policy of the theta loads
   uint32_t opaque_zero;     // always 0; the compiler cannot prove it (see BlockRegs::join)
@@ -108,7 +114,7 @@ __device__ __forceinline__ T make_stop(const DrawParams<T>& p, int64_t tok, T to
   if (p.stop_mode == WD_STOPS_EXPLICIT) {
     stop = p.stops[tok];
     bool live = total > T(0);
-    if (stop < T(0) || (live && stop >= total) || (!live && stop > T(0))) atomicOr(p.err + 1, 1ull);
+    if (stop < T(0) || (live && stop >= total) || (!live && stop > T(0))) atomicAnd(p.err + 1, 0ull);
     return stop;
   }
   T uf;
@@ -126,12 +132,77 @@ __device__ __forceinline__ T make_stop(const DrawParams<T>& p, int64_t tok, T to
 }
 
 // ============================================================== butterfly
+// 128-bit shared-memory moves of one E-element segment (16-byte aligned)
+__device__ __forceinline__ void store_seg(float* p, const float (&a)[4]) {
+  *reinterpret_cast<float4*>(p) = make_float4(a[0], a[1], a[2], a[3]);
+}
+__device__ __forceinline__ void store_seg(double* p, const double (&a)[4]) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(a[0], a[1]);
+  reinterpret_cast<double2*>(p)[1] = make_double2(a[2], a[3]);
+}
+template <typename T, int E>
+__device__ __forceinline__ void store_seg(T* p, const T (&a)[E]) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) p[e] = a[e];
+}
+__device__ __forceinline__ void load_seg_smem(float (&a)[4], const float* p) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+}
+__device__ __forceinline__ void load_seg_smem(double (&a)[4], const double* p) {
+  const double2 v0 = reinterpret_cast<const double2*>(p)[0], v1 = reinterpret_cast<const double2*>(p)[1];
+  a[0] = v0.x; a[1] = v0.y; a[2] = v1.x; a[3] = v1.y;
+}
+template <typename T, int E>
+__device__ __forceinline__ void load_seg_smem(T (&a)[E], const T* p) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) a[e] = p[e];
+}
+
+// the first n (< E) elements of a segment, scalar loads (tail of the remnant)
+template <typename T, int E>
+__device__ __forceinline__ void load_first(T (&v)[E], const T* __restrict__ p, int n) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = e < n ? __ldg(p + e) : T(0);
+}
+
+// Levels log2(E)+1 .. log2(W) of the block trees: transpose-reduce of the L
+// per-lane partial sums q over lanes s ^ 1, s ^ 2, ... (the paper's butterfly
+// exchange).  Afterwards the lane holds the block total of row s*R + lane/L.
+template <typename T, int L>
+__device__ __forceinline__ T xreduce(T (&q)[L], int s) {
+#pragma unroll
+  for (int bit = 1, n = L; bit < L; bit <<= 1, n >>= 1) {
+    const bool hi = (s & bit) != 0;
+#pragma unroll
+    for (int t = 0; t < n / 2; ++t) {
+      const T x0 = q[2 * t], x1 = q[2 * t + 1];
+      const T send = hi ? x0 : x1;
+      const T keep = hi ? x1 : x0;
+      q[t] = add_rn(keep, __shfl_xor_sync(FULL, send, bit));
+    }
+  }
+  return q[0];
+}
+
 __device__ __forceinline__ uint32_t lo_bits(float v) { return __float_as_uint(v); }
 __device__ __forceinline__ uint32_t lo_bits(double v) { return (uint32_t)__double_as_longlong(v); }
 __device__ __forceinline__ void or_bits(float& v, uint32_t d) { v = __uint_as_float(__float_as_uint(v) | d); }
 __device__ __forceinline__ void or_bits(double& v, uint32_t d) {
   v = __longlong_as_double(__double_as_longlong(v) | (long long)d);
 }
+
+// N row addresses kept as 32-bit row indices over one 64-bit column base
+// (row stride in bytes < 2^32): 1 register per row instead of 2, and one
+// IMAD.WIDE per load.
+template <typename T, int N> struct RowSet {
+  uint32_t idx[N];
+  const char* base;  // column base of row 0 (bytes)
+  uint32_t ldb;      // row stride in bytes
+  __device__ __forceinline__ const T* ptr(int i, int64_t off) const {
+    return reinterpret_cast<const T*>(base + (uint64_t)idx[i] * ldb) + off;
+  }
+};
 
 // One W-topic block of the 32-row chunk held in registers: L vector segments
 // of phi (or weights) per lane, plus theta segments: ND = 1 when every row of
@@ -145,13 +216,13 @@ template <typename T, int W, bool VEC, int MODE, int ND> struct BlockRegs {
   Seg<T, E, VEC> th[NT];
   // every load is unconditional (invalid rows point at a valid row) so all
   // of them are in flight before the first use
-  __device__ __forceinline__ void load(const T* const (&prow)[L], const T* const (&trow)[LT], int64_t off,
+  __device__ __forceinline__ void load(const RowSet<T, L>& P, const RowSet<T, LT>& Q, int64_t off,
                                        uint64_t pol_x, uint64_t pol_t) {
 #pragma unroll
-    for (int kk = 0; kk < L; ++kk) x[kk].load(prow[kk] + off, pol_x);
+    for (int kk = 0; kk < L; ++kk) x[kk].load(P.ptr(kk, off), pol_x);
     if (MODE == MODE_LDA) {
 #pragma unroll
-      for (int i = 0; i < NT; ++i) th[i].load(trow[i] + off, pol_t);
+      for (int i = 0; i < NT; ++i) th[i].load(Q.ptr(i, off), pol_t);
     }
   }
   // Make every consumer depend on EVERY load of the block (through an
@@ -192,20 +263,37 @@ template <typename T, int W, bool VEC, int MODE, int ND> struct BlockRegs {
       }
       q[kk] = rvalid[kk] ? Tree<T, E>::sum(a) : T(0);
     }
-#pragma unroll
-    for (int bit = 1, n = L; bit < L; bit <<= 1, n >>= 1) {
-      const bool hi = (s & bit) != 0;
-#pragma unroll
-      for (int t = 0; t < n / 2; ++t) {
-        const T x0 = q[2 * t], x1 = q[2 * t + 1];
-        const T send = hi ? x0 : x1;
-        const T keep = hi ? x1 : x0;
-        q[t] = add_rn(keep, __shfl_xor_sync(FULL, send, bit));
-      }
-    }
-    return q[0];
+    return xreduce<T, L>(q, s);
   }
 };
+
+// Rows from more than two documents (LDA, ND = 0): theta is loaded per row,
+// in two half batches so at most L/2 (phi, theta) pairs are live at once.
+template <typename T, int W, bool VEC>
+__device__ __forceinline__ T block_total_nd0(const RowSet<T, Geo<W>::L>& P,
+                                             const RowSet<T, (Geo<W>::L < 2 ? 2 : Geo<W>::L)>& Q, int64_t off,
+                                             const bool (&rvalid)[Geo<W>::L], int s, uint64_t px, uint64_t pt) {
+  constexpr int E = Geo<W>::E, L = Geo<W>::L;
+  constexpr int H = L >= 4 ? L / 2 : L;
+  T q[L];
+#pragma unroll
+  for (int h = 0; h < L; h += H) {
+    Seg<T, E, VEC> x[H], th[H];
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      x[j].load(P.ptr(h + j, off), px);
+      th[j].load(Q.ptr(h + j, off), pt);
+    }
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      T a[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) a[e] = mul_rn(th[j].v[e], x[j].v[e]);
+      q[h + j] = rvalid[h + j] ? Tree<T, E>::sum(a) : T(0);
+    }
+  }
+  return xreduce<T, L>(q, s);
+}
 
 // Pass 1 over all blocks: running block sums S_b of the own row
 // (sequential over blocks, kernels.py:221-223).  Memory-level parallelism:
@@ -213,13 +301,18 @@ template <typename T, int W, bool VEC, int MODE, int ND> struct BlockRegs {
 //   PIPE = 2  block b+1's loads issued before block b's arithmetic;
 //   PIPE = 3  two blocks' loads issued together, then both reduced.
 template <typename T, int W, bool VEC, int MODE, int ND, int PIPE>
-__device__ __forceinline__ T bfly_blocks(const T* const (&prow)[Geo<W>::L],
-                                         const T* const (&trow)[(Geo<W>::L < 2 ? 2 : Geo<W>::L)],
+__device__ __forceinline__ T bfly_blocks(const RowSet<T, Geo<W>::L>& prow,
+                                         const RowSet<T, (Geo<W>::L < 2 ? 2 : Geo<W>::L)>& trow,
                                          const bool (&rvalid)[Geo<W>::L], int nb, int s, T acc,
                                          T* __restrict__ S, int lane, uint64_t px, uint64_t pt,
                                          uint32_t opaque_zero, uint32_t dsel) {
   using R = BlockRegs<T, W, VEC, MODE, ND>;
-  if (PIPE == 1 || PIPE == 4) {
+  if (MODE == MODE_LDA && ND == 0 && PIPE != 4) {
+    for (int b = 0; b < nb; ++b) {
+      acc = add_rn(acc, block_total_nd0<T, W, VEC>(prow, trow, (int64_t)b * W, rvalid, s, px, pt));
+      S[b * 32 + lane] = acc;
+    }
+  } else if (PIPE == 1 || PIPE == 4) {
     for (int b = 0; b < nb; ++b) {
       R cur;
       cur.load(prow, trow, (int64_t)b * W, px, pt);
@@ -279,7 +372,10 @@ template <typename T> struct Walk<T, 0> {
 };
 
 template <typename T, int W, bool VEC, int MODE, int PIPE>
-__global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
+__global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC) ? (MODE == MODE_LDA ? WD_LDA_MIN_BLOCKS
+                                                                                 : (PIPE == 2 ? 4 : 8))
+                                                                        : 1)
+    bfly_kernel(DrawParams<T> p) {
   using G = Geo<W>;
   constexpr int E = G::E, L = G::L, R = G::R;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -287,7 +383,13 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
   const int wib = threadIdx.x >> 5;
   const int K = p.K;
   const int nb = K / W, rem = K % W;
+  const int wpb_i = blockDim.x >> 5;
   T* S = reinterpret_cast<T*>(smem_raw) + (size_t)wib * (size_t)(nb > 0 ? nb : 1) * 32;
+  // remnant tile [32 rows][TS] per warp (after every warp's S).  Vector path:
+  // stride W + 4 keeps rows 16-byte aligned and the 128-bit segment stores /
+  // row scans conflict-free; scalar path: odd stride W + 1.
+  constexpr int TS = VEC ? W + 4 : W + 1;
+  T* RT = reinterpret_cast<T*>(smem_raw) + (size_t)wpb_i * (size_t)(nb > 0 ? nb : 1) * 32 + (size_t)wib * 32 * TS;
   const int s = lane % L;
   const int rg = lane / L;
   const int own = s * R + rg;  // chunk row this lane ends up owning
@@ -304,8 +406,13 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
       my_doc = p.token_doc[tok0 + lane];
       my_word = p.words[tok0 + lane];
     }
-    const T* prow[L];
-    const T* trow[L];
+    constexpr int LT = L < 2 ? 2 : L;
+    RowSet<T, L> prow;  // the L rows this lane loads (phi / weights)
+    RowSet<T, LT> trow;  // their theta rows (LDA)
+    prow.base = reinterpret_cast<const char*>(p.phi + rem + s * E);
+    prow.ldb = (uint32_t)(p.ld_phi * sizeof(T));
+    trow.base = MODE == MODE_LDA ? reinterpret_cast<const char*>(p.theta + rem + s * E) : nullptr;
+    trow.ldb = (uint32_t)(p.ld_theta * sizeof(T));
     bool rvalid[L];
 #pragma unroll
     for (int kk = 0; kk < L; ++kk) {
@@ -313,15 +420,14 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
       rvalid[kk] = tok0 + k < n;
       if (MODE == MODE_LDA) {
         // invalid rows read word 0 / doc 0 (valid memory); their sums are discarded
-        const int32_t wk = __shfl_sync(FULL, my_word, k);
-        const int32_t dk = __shfl_sync(FULL, my_doc, k);
-        prow[kk] = p.phi + (int64_t)wk * p.ld_phi + rem + s * E;
-        trow[kk] = p.theta + (int64_t)dk * p.ld_theta + rem + s * E;
+        prow.idx[kk] = (uint32_t)__shfl_sync(FULL, my_word, k);
+        trow.idx[kk] = (uint32_t)__shfl_sync(FULL, my_doc, k);
       } else {
-        prow[kk] = p.phi + (rvalid[kk] ? tok0 + k : tok0) * p.ld_phi + rem + s * E;
-        trow[kk] = nullptr;
+        prow.idx[kk] = (uint32_t)(rvalid[kk] ? tok0 + k : tok0);
+        trow.idx[kk] = 0;
       }
     }
+    if (L < 2) trow.idx[LT - 1] = trow.idx[0];
     const int64_t own_tok = tok0 + own;
     const bool own_valid = own_tok < n;
     const int32_t own_doc = __shfl_sync(FULL, my_doc, own);
@@ -329,12 +435,53 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
     const T* pown = p.phi + (MODE == MODE_LDA ? (int64_t)own_word : own_tok) * p.ld_phi;
     const T* town = MODE == MODE_LDA ? p.theta + (int64_t)own_doc * p.ld_theta : nullptr;
 
-    // remnant: sequential running sums of the own row (kernels.py:199-205)
+    // remnant (topics [0, rem)): loaded cooperatively like a block, products
+    // staged in the warp's shared tile, then summed sequentially along the
+    // own row (kernels.py:199-205)
     T acc = T(0);
-    if (own_valid) {
-      for (int t = 0; t < rem; ++t) {
-        T a = MODE == MODE_LDA ? mul_rn(__ldg(town + t), __ldg(pown + t)) : __ldg(pown + t);
-        acc = add_rn(acc, a);
+    if (rem > 0) {
+      // half batches of rows keep the live loads (and the kernel's register
+      // budget) at the level of the block loop
+      constexpr int HB = L >= 4 ? L / 2 : L;
+#pragma unroll
+      for (int h = 0; h < L; h += HB) {
+#pragma unroll
+        for (int kk = h; kk < h + HB; ++kk) {
+          if (s * E < rem) {
+            const int k = kk * R + rg;
+            const bool full = s * E + E <= rem;  // else: partial segment, scalar loads
+            Seg<T, E, VEC> x;
+            if (full) x.load(prow.ptr(kk, -rem)); else load_first(x.v, prow.ptr(kk, -rem), rem - s * E);
+            T a[E];
+            if (MODE == MODE_LDA) {
+              Seg<T, E, VEC> th;
+              if (full) th.load(trow.ptr(kk, -rem)); else load_first(th.v, trow.ptr(kk, -rem), rem - s * E);
+#pragma unroll
+              for (int e = 0; e < E; ++e) a[e] = mul_rn(th.v[e], x.v[e]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < E; ++e) a[e] = x.v[e];
+            }
+            if (VEC && full) {
+              store_seg(RT + k * TS + s * E, a);
+            } else {
+#pragma unroll
+              for (int e = 0; e < E; ++e)
+                if (s * E + e < rem) RT[k * TS + s * E + e] = a[e];
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (VEC && rem % E == 0) {
+        for (int t = 0; t < rem; t += E) {
+          T a[E];
+          load_seg_smem(a, RT + own * TS + t);
+#pragma unroll
+          for (int e = 0; e < E; ++e) acc = add_rn(acc, a[e]);
+        }
+      } else {
+        for (int t = 0; t < rem; ++t) acc = add_rn(acc, RT[own * TS + t]);
       }
     }
     const T prem = acc;
@@ -343,10 +490,7 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
     // Chunks are CSR-ordered, so their documents are nondecreasing.
     int nd = 1;
     uint32_t dsel = 0;
-    const T* trow_nd[L < 2 ? 2 : L];
-#pragma unroll
-    for (int kk = 0; kk < L; ++kk) trow_nd[kk] = trow[kk];
-    if (L < 2) trow_nd[L < 2 ? 1 : 0] = trow[0];
+    RowSet<T, LT> trow_nd = trow;
     if (MODE == MODE_LDA) {
       const int32_t d0 = __shfl_sync(FULL, my_doc, 0);
       const int32_t d1 = __reduce_max_sync(FULL, my_valid ? my_doc : d0);
@@ -358,22 +502,27 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
             const int32_t dk = __shfl_sync(FULL, my_doc, kk * R + rg);
             if (dk == d1 && rvalid[kk]) dsel |= 1u << kk;
           }
-          trow_nd[0] = p.theta + (int64_t)d0 * p.ld_theta + rem + s * E;
-          trow_nd[1] = p.theta + (int64_t)d1 * p.ld_theta + rem + s * E;
+          trow_nd.idx[0] = (uint32_t)d0;
+          trow_nd.idx[1] = (uint32_t)d1;
         }
       } else {
-        trow_nd[0] = p.theta + (int64_t)d0 * p.ld_theta + rem + s * E;
+        trow_nd.idx[0] = (uint32_t)d0;
       }
     }
-    if (nd == 1)
+    if constexpr (MODE == MODE_ROWS) {
       acc = bfly_blocks<T, W, VEC, MODE, 1, PIPE>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
                                                   p.opaque_zero, 0u);
-    else if (MODE == MODE_LDA && nd == 2)
-      acc = bfly_blocks<T, W, VEC, MODE, 2, PIPE>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
-                                                  p.opaque_zero, dsel);
-    else  // >2 documents: L theta segments per block, no room to double-buffer
-      acc = bfly_blocks<T, W, VEC, MODE, 0, (MODE == MODE_LDA && PIPE != 4 ? 1 : PIPE)>(
-          prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t, p.opaque_zero, 0u);
+    } else {
+      if (nd == 1)
+        acc = bfly_blocks<T, W, VEC, MODE, 1, PIPE>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
+                                                    p.opaque_zero, 0u);
+      else if (nd == 2)
+        acc = bfly_blocks<T, W, VEC, MODE, 2, PIPE>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
+                                                    p.opaque_zero, dsel);
+      else  // >2 documents: per-row theta segments
+        acc = bfly_blocks<T, W, VEC, MODE, 0, (PIPE != 4 ? 1 : PIPE)>(prow, trow_nd, rvalid, nb, s, acc, S, lane,
+                                                                      pol_x, pol_t, p.opaque_zero, 0u);
+    }
     __syncwarp();
     const T total = acc;
 
@@ -396,20 +545,26 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
       const bool fallback = bb > 0 && stop < prev && total > T(0);
       int result = 0;
       if (nb > 0 && !fallback) {
-        // rebuild the selected block's products (own row) and walk it
+        // rebuild the selected block's products (own row) and walk it; the
+        // loads go in two halves to bound live registers
         T cur[W];
+        constexpr int NG = W / E;
+        constexpr int HG = NG >= 4 ? NG / 2 : NG;
 #pragma unroll
-        for (int g = 0; g < W / E; ++g) {
-          Seg<T, E, VEC> x;
-          x.load(pown + bb + g * E);
-          if (MODE == MODE_LDA) {
-            Seg<T, E, VEC> th;
-            th.load(town + bb + g * E);
+        for (int h = 0; h < NG; h += HG) {
 #pragma unroll
-            for (int e = 0; e < E; ++e) cur[g * E + e] = mul_rn(th.v[e], x.v[e]);
-          } else {
+          for (int g = h; g < h + HG; ++g) {
+            Seg<T, E, VEC> x;
+            x.load(pown + bb + g * E);
+            if (MODE == MODE_LDA) {
+              Seg<T, E, VEC> th;
+              th.load(town + bb + g * E);
 #pragma unroll
-            for (int e = 0; e < E; ++e) cur[g * E + e] = x.v[e];
+              for (int e = 0; e < E; ++e) cur[g * E + e] = mul_rn(th.v[e], x.v[e]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < E; ++e) cur[g * E + e] = x.v[e];
+            }
           }
         }
         T low = prev, high = S[j * 32 + lane];
@@ -418,11 +573,10 @@ __global__ void __launch_bounds__(128) bfly_kernel(DrawParams<T> p) {
         result = (int)bb + lo;
       }
       if (fallback) {
-        // linear remnant fallback (kernels.py:354-361)
+        // linear remnant fallback (kernels.py:354-361), products from the tile
         T a2 = T(0);
         for (int t = 0; t < rem; ++t) {
-          T a = MODE == MODE_LDA ? mul_rn(__ldg(town + t), __ldg(pown + t)) : __ldg(pown + t);
-          a2 = add_rn(a2, a);
+          a2 = add_rn(a2, RT[own * TS + t]);
           if (stop < a2) { result = t; break; }
         }
       }

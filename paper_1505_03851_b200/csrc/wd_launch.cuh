@@ -38,11 +38,13 @@ inline int occupancy_blocks(const void* fn, size_t smem, int threads = kThreads)
   return nb;
 }
 
-// shared memory of one warp's running block sums S[b][lane]
+// shared memory of one warp: running block sums S[b][lane] + remnant tile
 template <typename T>
 inline size_t bfly_smem_per_warp(int W, int K) {
   int nb = K / W;
-  return (size_t)(nb > 0 ? nb : 1) * 32 * sizeof(T);
+  size_t b = (size_t)(nb > 0 ? nb : 1) * 32 * sizeof(T);
+  if (K % W) b += (size_t)32 * (W + 4) * sizeof(T);
+  return b;
 }
 template <typename T>
 inline size_t prefix_smem() {
@@ -95,7 +97,7 @@ int launch_bfly_inst(const DrawParams<T>& p0, cudaStream_t st) {
   DrawParams<T> p = p0;
   l2_policies(MODE, p.l2_policy_x, p.l2_policy_t);
   // the multi-block variants are instantiated for the fp32 W=32 vector path only
-  if (std::is_same<T, float>::value && W == 32 && VEC) {
+  if constexpr (std::is_same<T, float>::value && W == 32 && VEC) {
     const int v = pipe_variant(MODE);
     if (v == 2) return launch_bfly_pipe<T, W, VEC, MODE, 2>(p, st);
     if (v == 3) return launch_bfly_pipe<T, W, VEC, MODE, 3>(p, st);

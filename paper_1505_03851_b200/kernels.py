@@ -312,7 +312,7 @@ def _stop_args(stops, corpus: DeviceCorpus, key_rule: int, lanes: int, device):
 
 
 def raise_for_err(err_host, key_rule: int, lanes: int):
-    allzero, stop_bad = int(err_host[0]), int(err_host[1])
+    allzero, stop_bad = int(err_host[0]), int(err_host[1]) != _lib.ERR_NONE
     if stop_bad:
         raise StopOutOfRangeError("stop values must lie in [0, sum)")
     if allzero != _lib.ERR_NONE:
@@ -389,7 +389,7 @@ def draw_z_device(kernel: str, corpus: DeviceCorpus, theta, phi, stops, lanes: i
 def combine_err(err) -> np.ndarray:
     """Fold per-launch error words [n, 2] into one (min AllZero key, any range flag)."""
     e = err.reshape(-1, 2).cpu().numpy().view(np.uint64)
-    return np.array([e[:, 0].min(), e[:, 1].max()], dtype=np.uint64)
+    return np.array([e[:, 0].min(), e[:, 1].min()], dtype=np.uint64)
 
 
 def _to_host_ragged(z_dev, N):

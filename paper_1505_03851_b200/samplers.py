@@ -14,7 +14,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from .kernels import StopOutOfRangeError
+from .kernels import StopOutOfRangeError, _workspace
 from .rng import derive_seed
 from .sampling import AllZeroError
 
@@ -75,15 +75,14 @@ def sample_rows(weights, seed: int | None = None, *, lanes: int = 32, variant: s
         err = torch.empty(2, dtype=torch.int64, device=dev)
     L = _lib.load()
     v = _VARIANTS[variant]
-    nbytes = int(L.wd_workspace_bytes(v, dt, int(lanes), K))
-    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev) if nbytes else None
+    ws, nbytes = _workspace(v, dt, int(lanes), K, dev)
     _lib.check(L.wd_sample_rows(v, dt, int(lanes), weights.data_ptr(), ld, n, K, int(row_base), mode,
                                 int(sd) & ((1 << 64) - 1), _lib.ptr(u_t), _lib.ptr(s_t), out.data_ptr(),
                                 err.data_ptr(), _lib.ptr(ws), nbytes, _lib.stream_handle(stream)),
                "wd_sample_rows")
     if check:
         e = err.cpu().numpy().view(np.uint64)
-        if int(e[1]):
+        if int(e[1]) != _lib.ERR_NONE:
             raise StopOutOfRangeError("stop values must lie in [0, sum)")
         if int(e[0]) != _lib.ERR_NONE and stops is None:
             raise AllZeroError(f"row {int(e[0])}: all weights are zero")

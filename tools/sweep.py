@@ -2,8 +2,9 @@
 
     python tools/sweep.py [--out profiles/sweep_r01] [--rows 1048576] [--docs 200000]
 
-Two sweeps, CUDA-event timed (3 warm-up + 10 timed launches, inputs larger
-than L2 or L2 flushed by a 256 MB write before each launch):
+Two sweeps, CUDA-event timed over a CUDA graph of 10 launches (3 warm-up
+launches first; inputs larger than L2, or L2 flushed by a 256 MB write before
+each launch with the flush time subtracted):
   * standalone independent rows (BASELINE configs[1]): n rows of K fp32
     weights, algorithmic bytes 4K + 4 per draw;
   * LDA z draw (configs[2] shape, scaled to --docs documents): butterfly vs
@@ -25,21 +26,42 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1505_03851_b200 as wd  # noqa: E402
 
 
+def _graph(body, iters):
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(iters):
+            body()
+    return g
+
+
+def _replay_ms(g):
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b)
+
+
 def timed(fn, flush, iters=10, warm=3):
+    """Device time per call: `iters` calls captured in one CUDA graph (no host
+    launch overhead in the measurement); with `flush`, a 256 MB write before
+    every call evicts L2 and its own time is subtracted."""
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
-    tot = 0.0
-    for _ in range(iters):
-        if flush is not None:
-            flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+    if flush is None:
+        return _replay_ms(_graph(fn, iters)) / iters / 1e3
+
+    def body():
+        flush.zero_()
         fn()
-        b.record()
-        torch.cuda.synchronize()
-        tot += a.elapsed_time(b)
-    return tot / iters / 1e3
+
+    t_all = _replay_ms(_graph(body, iters))
+    t_flush = _replay_ms(_graph(flush.zero_, iters))
+    return (t_all - t_flush) / iters / 1e3
 
 
 def main():
@@ -84,9 +106,13 @@ def main():
         theta = torch.rand((M, K), generator=g, device="cuda") * 0.9 + 0.1
         phi = torch.rand((V, K), generator=g, device="cuda") * 0.9 + 0.1
         r = {"K": K}
+        # the product's default: vocabulary tiles when phi exceeds ~40 MB (DeviceLDA)
+        tiles = dc.vocab_tiles((40 << 20) // (4 * K)) if V * K * 4 > (40 << 20) else None
+        r["vocab_tiles"] = tiles.n_tiles if tiles else 1
+        terr = torch.empty((r["vocab_tiles"], 2), dtype=torch.int64, device="cuda")
         for kern in ("butterfly", "transposed"):
-            dt = timed(lambda: wd.draw_z_device(kern, dc, theta, phi, wd.SeededStops(3), 32, z=z, err=err,
-                                                check=False), flush, iters=5, warm=2)
+            dt = timed(lambda: wd.draw_z_device(kern, dc, theta, phi, wd.SeededStops(3), 32, z=z, err=terr,
+                                                check=False, tiles=tiles), flush, iters=5, warm=2)
             r[kern] = {"ms": dt * 1e3, "tokens_per_s": T / dt,
                        "alg_GBps": T * (4 * K + 4 * K * M / T + 8) / dt / 1e9}
         r["speedup"] = r["transposed"]["ms"] / r["butterfly"]["ms"]
@@ -105,11 +131,11 @@ def main():
             fh.write(f"| {r['K']} | {r['butterfly']['draws_per_s']:.3e} | {r['butterfly']['frac']:.2f} | "
                      f"{r['prefix']['draws_per_s']:.3e} | {r['prefix']['frac']:.2f} | {r['speedup']:.2f}x |\n")
         fh.write(f"\nLDA z draw: {M} docs, {T} tokens (Poisson(200)), V = {V}, fp32, W = 32.\n\n")
-        fh.write("| K | butterfly tokens/s | alg. GB/s | prefix-table (transposed) tokens/s | speedup |\n"
-                 "|---|---|---|---|---|\n")
+        fh.write("| K | vocab tiles | butterfly tokens/s | alg. GB/s | prefix-table (transposed) tokens/s | speedup |\n"
+                 "|---|---|---|---|---|---|\n")
         for r in lda:
-            fh.write(f"| {r['K']} | {r['butterfly']['tokens_per_s']:.3e} | {r['butterfly']['alg_GBps']:.0f} | "
-                     f"{r['transposed']['tokens_per_s']:.3e} | {r['speedup']:.2f}x |\n")
+            fh.write(f"| {r['K']} | {r['vocab_tiles']} | {r['butterfly']['tokens_per_s']:.3e} | "
+                     f"{r['butterfly']['alg_GBps']:.0f} | {r['transposed']['tokens_per_s']:.3e} | {r['speedup']:.2f}x |\n")
     print("wrote", a.out + ".md")
 
 
