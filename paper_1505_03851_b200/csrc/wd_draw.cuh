@@ -132,6 +132,14 @@ __device__ __forceinline__ T make_stop(const DrawParams<T>& p, int64_t tok, T to
 }
 
 // ============================================================== butterfly
+// cp.async (LDGSTS): 16-byte global -> shared copies that hold no registers
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 // 128-bit shared-memory moves of one E-element segment (16-byte aligned)
 __device__ __forceinline__ void store_seg(float* p, const float (&a)[4]) {
   *reinterpret_cast<float4*>(p) = make_float4(a[0], a[1], a[2], a[3]);
@@ -305,11 +313,14 @@ __device__ __forceinline__ T bfly_blocks(const RowSet<T, Geo<W>::L>& prow,
                                          const RowSet<T, (Geo<W>::L < 2 ? 2 : Geo<W>::L)>& trow,
                                          const bool (&rvalid)[Geo<W>::L], int nb, int s, T acc,
                                          T* __restrict__ S, int lane, uint64_t px, uint64_t pt,
-                                         uint32_t opaque_zero, uint32_t dsel) {
+                                         uint32_t opaque_zero, uint32_t dsel, bool raw) {
+  // raw: store the block totals T_b themselves (the running sums are formed
+  // after the remnant prefix is known); else S_b = S_{b-1} + T_b directly
   using R = BlockRegs<T, W, VEC, MODE, ND>;
   if (MODE == MODE_LDA && ND == 0 && PIPE != 4) {
     for (int b = 0; b < nb; ++b) {
-      acc = add_rn(acc, block_total_nd0<T, W, VEC>(prow, trow, (int64_t)b * W, rvalid, s, px, pt));
+      const T t = block_total_nd0<T, W, VEC>(prow, trow, (int64_t)b * W, rvalid, s, px, pt);
+      acc = raw ? t : add_rn(acc, t);
       S[b * 32 + lane] = acc;
     }
   } else if (PIPE == 1 || PIPE == 4) {
@@ -317,7 +328,8 @@ __device__ __forceinline__ T bfly_blocks(const RowSet<T, Geo<W>::L>& prow,
       R cur;
       cur.load(prow, trow, (int64_t)b * W, px, pt);
       if (PIPE == 4) cur.join(opaque_zero);
-      acc = add_rn(acc, cur.reduce(rvalid, s, dsel));
+      const T t = cur.reduce(rvalid, s, dsel);
+      acc = raw ? t : add_rn(acc, t);
       S[b * 32 + lane] = acc;
     }
   } else if (PIPE == 2) {
@@ -326,7 +338,8 @@ __device__ __forceinline__ T bfly_blocks(const RowSet<T, Geo<W>::L>& prow,
     for (int b = 0; b < nb; ++b) {
       R nxt;
       if (b + 1 < nb) nxt.load(prow, trow, (int64_t)(b + 1) * W, px, pt);
-      acc = add_rn(acc, cur.reduce(rvalid, s, dsel));
+      const T t = cur.reduce(rvalid, s, dsel);
+      acc = raw ? t : add_rn(acc, t);
       S[b * 32 + lane] = acc;
       cur = nxt;
     }
@@ -336,15 +349,18 @@ __device__ __forceinline__ T bfly_blocks(const RowSet<T, Geo<W>::L>& prow,
       R c0, c1;
       c0.load(prow, trow, (int64_t)b * W, px, pt);
       c1.load(prow, trow, (int64_t)(b + 1) * W, px, pt);
-      acc = add_rn(acc, c0.reduce(rvalid, s, dsel));
+      const T t0 = c0.reduce(rvalid, s, dsel);
+      acc = raw ? t0 : add_rn(acc, t0);
       S[b * 32 + lane] = acc;
-      acc = add_rn(acc, c1.reduce(rvalid, s, dsel));
+      const T t1 = c1.reduce(rvalid, s, dsel);
+      acc = raw ? t1 : add_rn(acc, t1);
       S[(b + 1) * 32 + lane] = acc;
     }
     if (b < nb) {
       R c0;
       c0.load(prow, trow, (int64_t)b * W, px, pt);
-      acc = add_rn(acc, c0.reduce(rvalid, s, dsel));
+      const T t0 = c0.reduce(rvalid, s, dsel);
+      acc = raw ? t0 : add_rn(acc, t0);
       S[b * 32 + lane] = acc;
     }
   }
@@ -435,11 +451,26 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC) ? (MOD
     const T* pown = p.phi + (MODE == MODE_LDA ? (int64_t)own_word : own_tok) * p.ld_phi;
     const T* town = MODE == MODE_LDA ? p.theta + (int64_t)own_doc * p.ld_theta : nullptr;
 
-    // remnant (topics [0, rem)): loaded cooperatively like a block, products
-    // staged in the warp's shared tile, then summed sequentially along the
-    // own row (kernels.py:199-205)
+    // remnant (topics [0, rem)), loaded cooperatively like a block into the
+    // warp's shared tiles and summed sequentially along the own row
+    // (kernels.py:199-205).  Vector path: cp.async copies issued now, consumed
+    // after the block loop, so the remnant costs no extra memory round trip;
+    // the block loop then stores raw block totals and the running sums are
+    // formed once the remnant prefix is known (same IEEE additions).
     T acc = T(0);
-    if (rem > 0) {
+    const bool async_rem = VEC && rem > 0 && rem % E == 0 && (E * sizeof(T)) % 16 == 0;
+    if (async_rem) {
+#pragma unroll
+      for (int kk = 0; kk < L; ++kk) {
+        if (s * E < rem) {
+          const int k = kk * R + rg;
+#pragma unroll
+          for (int c = 0; c < (int)(E * sizeof(T) / 16); ++c)
+            cp_async16(RT + k * TS + s * E + c * (16 / sizeof(T)), prow.ptr(kk, -rem + c * (16 / (int)sizeof(T))));
+        }
+      }
+      cp_async_commit();
+    } else if (rem > 0) {
       // half batches of rows keep the live loads (and the kernel's register
       // budget) at the level of the block loop
       constexpr int HB = L >= 4 ? L / 2 : L;
@@ -462,29 +493,13 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC) ? (MOD
 #pragma unroll
               for (int e = 0; e < E; ++e) a[e] = x.v[e];
             }
-            if (VEC && full) {
-              store_seg(RT + k * TS + s * E, a);
-            } else {
 #pragma unroll
-              for (int e = 0; e < E; ++e)
-                if (s * E + e < rem) RT[k * TS + s * E + e] = a[e];
-            }
+            for (int e = 0; e < E; ++e)
+              if (s * E + e < rem) RT[k * TS + s * E + e] = a[e];
           }
         }
       }
-      __syncwarp();
-      if (VEC && rem % E == 0) {
-        for (int t = 0; t < rem; t += E) {
-          T a[E];
-          load_seg_smem(a, RT + own * TS + t);
-#pragma unroll
-          for (int e = 0; e < E; ++e) acc = add_rn(acc, a[e]);
-        }
-      } else {
-        for (int t = 0; t < rem; ++t) acc = add_rn(acc, RT[own * TS + t]);
-      }
     }
-    const T prem = acc;
     // theta rows the chunk needs: one document (ND=1), two (ND=2: the rows of
     // the second one are flagged in dsel), or more (ND=0: per-row loads).
     // Chunks are CSR-ordered, so their documents are nondecreasing.
@@ -511,17 +526,45 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC) ? (MOD
     }
     if constexpr (MODE == MODE_ROWS) {
       acc = bfly_blocks<T, W, VEC, MODE, 1, PIPE>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
-                                                  p.opaque_zero, 0u);
+                                                  p.opaque_zero, 0u, rem > 0);
     } else {
       if (nd == 1)
         acc = bfly_blocks<T, W, VEC, MODE, 1, PIPE>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
-                                                    p.opaque_zero, 0u);
+                                                    p.opaque_zero, 0u, rem > 0);
       else if (nd == 2)
         acc = bfly_blocks<T, W, VEC, MODE, 2, PIPE>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
-                                                    p.opaque_zero, dsel);
+                                                    p.opaque_zero, dsel, rem > 0);
       else  // >2 documents: per-row theta segments
         acc = bfly_blocks<T, W, VEC, MODE, 0, (PIPE != 4 ? 1 : PIPE)>(prow, trow_nd, rvalid, nb, s, acc, S, lane,
-                                                                      pol_x, pol_t, p.opaque_zero, 0u);
+                                                                      pol_x, pol_t, p.opaque_zero, 0u, rem > 0);
+    }
+    T prem = T(0);
+    if (rem > 0) {
+      if (async_rem) cp_async_wait_all();
+      __syncwarp();
+      // sequential remnant prefix of the own row (products formed here on the
+      // asynchronous path, already in the tile on the synchronous one)
+      if (async_rem) {
+        for (int t = 0; t < rem; t += E) {
+          T a[E];
+          load_seg_smem(a, RT + own * TS + t);
+          if (MODE == MODE_LDA) {  // the own document's theta remnant (L1-resident)
+            Seg<T, E, VEC> th;
+            th.load(town + t);
+#pragma unroll
+            for (int e = 0; e < E; ++e) a[e] = mul_rn(th.v[e], a[e]);
+          }
+#pragma unroll
+          for (int e = 0; e < E; ++e) prem = add_rn(prem, a[e]);
+        }
+      } else {
+        for (int t = 0; t < rem; ++t) prem = add_rn(prem, RT[own * TS + t]);
+      }
+      acc = prem;
+      for (int b = 0; b < nb; ++b) {  // S_b = S_{b-1} + T_b from the raw totals
+        acc = add_rn(acc, S[b * 32 + lane]);
+        S[b * 32 + lane] = acc;
+      }
     }
     __syncwarp();
     const T total = acc;
@@ -573,10 +616,11 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC) ? (MOD
         result = (int)bb + lo;
       }
       if (fallback) {
-        // linear remnant fallback (kernels.py:354-361), products from the tile
+        // linear remnant fallback (kernels.py:354-361), products from the tile(s)
         T a2 = T(0);
         for (int t = 0; t < rem; ++t) {
-          a2 = add_rn(a2, RT[own * TS + t]);
+          const T a = (MODE == MODE_LDA && async_rem) ? mul_rn(__ldg(town + t), RT[own * TS + t]) : RT[own * TS + t];
+          a2 = add_rn(a2, a);
           if (stop < a2) { result = t; break; }
         }
       }

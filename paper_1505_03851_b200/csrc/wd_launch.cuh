@@ -40,7 +40,7 @@ inline int occupancy_blocks(const void* fn, size_t smem, int threads = kThreads)
 
 // shared memory of one warp: running block sums S[b][lane] + remnant tile
 template <typename T>
-inline size_t bfly_smem_per_warp(int W, int K) {
+inline size_t bfly_smem_per_warp(int W, int K, int mode) {
   int nb = K / W;
   size_t b = (size_t)(nb > 0 ? nb : 1) * 32 * sizeof(T);
   if (K % W) b += (size_t)32 * (W + 4) * sizeof(T);
@@ -73,7 +73,7 @@ inline void l2_policies(int mode, int& px, int& pt) {
 template <typename T, int W, bool VEC, int MODE, int PIPE>
 int launch_bfly_pipe(const DrawParams<T>& p, cudaStream_t st) {
   const void* fn = (const void*)bfly_kernel<T, W, VEC, MODE, PIPE>;
-  const size_t per_warp = bfly_smem_per_warp<T>(W, p.K);
+  const size_t per_warp = bfly_smem_per_warp<T>(W, p.K, MODE);
   int wpb = kThreads / 32;  // fewer warps per CTA when the block sums are large
   while (wpb > 1 && (size_t)wpb * per_warp > 227 * 1024) wpb >>= 1;
   const size_t smem = (size_t)wpb * per_warp;
