@@ -148,9 +148,9 @@ int wd_topic_counts(const int32_t* words, const int32_t* token_doc, const int32_
 
 /*
  * Throughput-mode Dirichlet resample (lda.py:185-208), statistical parity:
- * Gammas from a counter-based stream (SplitMix64 finalizer over a Weyl
- * counter) keyed by (seed, row, topic, attempt), Marsaglia-Tsang in log
- * space, deterministic reductions.
+ * Gammas from a counter-based stream (32-bit integer hash of a counter)
+ * keyed by (seed, row, topic, attempt), Marsaglia-Tsang in log space,
+ * deterministic reductions.
  *   wd_resample_theta: theta[m, :] ~ Dir(alpha + histogram of z over doc m)
  *     (the doc-topic counts are formed in shared memory, never in HBM);
  *     row key = doc_base + m.

@@ -367,6 +367,69 @@ __device__ __forceinline__ T bfly_blocks(const RowSet<T, Geo<W>::L>& prow,
   return acc;
 }
 
+// Ring depth of the cp.async block pipeline (PIPE 5 -> 3 stages, 6 -> 4).
+template <int PIPE> struct RingDepth { static constexpr int NS = PIPE == 6 ? 4 : 3; };
+// cp.async wait with a compile-time group count
+template <int N> __device__ __forceinline__ void cp_async_wait_n() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+// bytes of one ring stage: L phi segments + up to 2 theta segments, 16 B per lane
+template <int W> struct RingStage { static constexpr int BYTES = (Geo<W>::L + 2) * 32 * 16; };
+
+// Pass 1 with the block loads staged through a per-warp shared-memory ring by
+// cp.async (fp32, 16-byte segments): block b+NS-1 is in flight while block b
+// is reduced, and in-flight data occupies shared memory instead of
+// registers.  Each lane reads back only the segments it copied itself, so the
+// per-thread wait_group is the only synchronisation needed.
+template <typename T, int W, int MODE, int ND, int NS>
+__device__ __forceinline__ T bfly_blocks_ring(const RowSet<T, Geo<W>::L>& prow,
+                                              const RowSet<T, (Geo<W>::L < 2 ? 2 : Geo<W>::L)>& trow,
+                                              const bool (&rvalid)[Geo<W>::L], int nb, int s, T acc,
+                                              T* __restrict__ S, int lane, uint32_t dsel, bool raw,
+                                              char* __restrict__ ring) {
+  static_assert(sizeof(T) * Geo<W>::E == 16, "ring path needs 16-byte segments");
+  constexpr int L = Geo<W>::L;
+  constexpr int NT = MODE == MODE_LDA ? ND : 0;
+  constexpr int STAGE = RingStage<W>::BYTES;
+  using R = BlockRegs<T, W, true, MODE, (MODE == MODE_LDA ? ND : 1)>;
+  auto issue = [&](int b) {
+    char* st = ring + (b % NS) * STAGE + lane * 16;
+#pragma unroll
+    for (int kk = 0; kk < L; ++kk) cp_async16(st + kk * 512, prow.ptr(kk, (int64_t)b * W));
+#pragma unroll
+    for (int i = 0; i < NT; ++i) cp_async16(st + (L + i) * 512, trow.ptr(i, (int64_t)b * W));
+  };
+#pragma unroll
+  for (int b = 0; b < NS - 1; ++b) {
+    if (b < nb) issue(b);
+    cp_async_commit();
+  }
+  for (int b = 0; b < nb; ++b) {
+    if (b + NS - 1 < nb) issue(b + NS - 1);
+    cp_async_commit();
+    cp_async_wait_n<NS - 1>();  // block b's group has landed
+    const char* st = ring + (b % NS) * STAGE + lane * 16;
+    R cur;
+#pragma unroll
+    for (int kk = 0; kk < L; ++kk) {
+      const float4 v = *reinterpret_cast<const float4*>(st + kk * 512);
+      cur.x[kk].v[0] = v.x; cur.x[kk].v[1] = v.y; cur.x[kk].v[2] = v.z; cur.x[kk].v[3] = v.w;
+    }
+    if (MODE == MODE_LDA) {
+#pragma unroll
+      for (int i = 0; i < R::NT; ++i) {
+        const float4 v = *reinterpret_cast<const float4*>(st + (L + i) * 512);
+        cur.th[i].v[0] = v.x; cur.th[i].v[1] = v.y; cur.th[i].v[2] = v.z; cur.th[i].v[3] = v.w;
+      }
+    }
+    const T t = cur.reduce(rvalid, s, dsel);
+    acc = raw ? t : add_rn(acc, t);
+    S[b * 32 + lane] = acc;
+  }
+  cp_async_wait_n<0>();
+  return acc;
+}
+
 // In-block walk (kernels.py:268-314).  Per level the reference compares stop
 // with low + node(lo, lo+bit-1) or with high - node(lo+bit, lo+2bit-1), picked
 // by bit `bit` of r = doc mod W; the nodes are the block's pairwise-tree nodes
@@ -388,9 +451,9 @@ template <typename T> struct Walk<T, 0> {
 };
 
 template <typename T, int W, bool VEC, int MODE, int PIPE>
-__global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC) ? (MODE == MODE_LDA ? WD_LDA_MIN_BLOCKS
-                                                                                 : (PIPE == 2 ? 4 : 8))
-                                                                        : 1)
+__global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
+                                             ? (PIPE == 2 ? 4 : (MODE == MODE_LDA ? WD_LDA_MIN_BLOCKS : 8))
+                                             : 1)
     bfly_kernel(DrawParams<T> p) {
   using G = Geo<W>;
   constexpr int E = G::E, L = G::L, R = G::R;
@@ -406,6 +469,11 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC) ? (MOD
   // row scans conflict-free; scalar path: odd stride W + 1.
   constexpr int TS = VEC ? W + 4 : W + 1;
   T* RT = reinterpret_cast<T*>(smem_raw) + (size_t)wpb_i * (size_t)(nb > 0 ? nb : 1) * 32 + (size_t)wib * 32 * TS;
+  // cp.async ring (PIPE 5/6), after every warp's S and remnant tile
+  constexpr bool RING = PIPE >= 5;
+  char* ring = reinterpret_cast<char*>(reinterpret_cast<T*>(smem_raw) + (size_t)wpb_i * (size_t)(nb > 0 ? nb : 1) * 32 +
+                                       (size_t)wpb_i * 32 * TS) +
+               (size_t)wib * RingDepth<PIPE>::NS * RingStage<W>::BYTES;
   const int s = lane % L;
   const int rg = lane / L;
   const int own = s * R + rg;  // chunk row this lane ends up owning
@@ -524,7 +592,17 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC) ? (MOD
         trow_nd.idx[0] = (uint32_t)d0;
       }
     }
-    if constexpr (MODE == MODE_ROWS) {
+    if constexpr (RING) {
+      if (MODE == MODE_ROWS || nd == 1)
+        acc = bfly_blocks_ring<T, W, MODE, 1, RingDepth<PIPE>::NS>(prow, trow_nd, rvalid, nb, s, acc, S, lane, 0u,
+                                                                   rem > 0, ring);
+      else if (nd == 2)
+        acc = bfly_blocks_ring<T, W, MODE, 2, RingDepth<PIPE>::NS>(prow, trow_nd, rvalid, nb, s, acc, S, lane, dsel,
+                                                                   rem > 0, ring);
+      else  // >2 documents: per-row theta segments, register path
+        acc = bfly_blocks<T, W, VEC, MODE, 0, 1>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
+                                                 p.opaque_zero, 0u, rem > 0);
+    } else if constexpr (MODE == MODE_ROWS) {
       acc = bfly_blocks<T, W, VEC, MODE, 1, PIPE>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
                                                   p.opaque_zero, 0u, rem > 0);
     } else {

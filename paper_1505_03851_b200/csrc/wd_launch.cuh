@@ -40,10 +40,11 @@ inline int occupancy_blocks(const void* fn, size_t smem, int threads = kThreads)
 
 // shared memory of one warp: running block sums S[b][lane] + remnant tile
 template <typename T>
-inline size_t bfly_smem_per_warp(int W, int K, int mode) {
+inline size_t bfly_smem_per_warp(int W, int K, int mode, int pipe = 1) {
   int nb = K / W;
   size_t b = (size_t)(nb > 0 ? nb : 1) * 32 * sizeof(T);
-  if (K % W) b += (size_t)32 * (W + 4) * sizeof(T);
+  if (K % W || pipe >= 5) b += (size_t)32 * (W + 4) * sizeof(T);  // remnant tile (the ring sits after it)
+  if (pipe >= 5) b += (size_t)(pipe == 6 ? 4 : 3) * ((W >= 4 ? W / 4 : 1) + 2) * 32 * 16;  // cp.async ring
   return b;
 }
 template <typename T>
@@ -58,10 +59,14 @@ inline int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return (e && e[0]) ? atoi(e) : dflt;
 }
-inline int pipe_variant(int mode) {
-  static int rows = env_int("WD_PIPE_ROWS", 2);
+inline int pipe_variant(int mode, int nb) {
+  // measured (profiles/): standalone rows -> cp.async ring (5) once there
+  // are >= 16 blocks per row, software pipelining (2) below; LDA -> one
+  // block of register loads in flight (1): its gathers need the warps
+  static int rows = env_int("WD_PIPE_ROWS", 0);
   static int lda = env_int("WD_PIPE_LDA", 1);
-  return mode == MODE_ROWS ? rows : lda;
+  if (mode == MODE_ROWS) return rows ? rows : ((nb >= 16 && nb <= 64) ? 5 : 2);
+  return lda >= 5 ? 1 : lda;  // the ring does not pay for the LDA gathers (occupancy)
 }
 // L2 policies (0 normal, 1 evict_last, 2 evict_first); WD_L2_X / WD_L2_T override
 inline void l2_policies(int mode, int& px, int& pt) {
@@ -73,7 +78,7 @@ inline void l2_policies(int mode, int& px, int& pt) {
 template <typename T, int W, bool VEC, int MODE, int PIPE>
 int launch_bfly_pipe(const DrawParams<T>& p, cudaStream_t st) {
   const void* fn = (const void*)bfly_kernel<T, W, VEC, MODE, PIPE>;
-  const size_t per_warp = bfly_smem_per_warp<T>(W, p.K, MODE);
+  const size_t per_warp = bfly_smem_per_warp<T>(W, p.K, MODE, PIPE);
   int wpb = kThreads / 32;  // fewer warps per CTA when the block sums are large
   while (wpb > 1 && (size_t)wpb * per_warp > 227 * 1024) wpb >>= 1;
   const size_t smem = (size_t)wpb * per_warp;
@@ -98,10 +103,12 @@ int launch_bfly_inst(const DrawParams<T>& p0, cudaStream_t st) {
   l2_policies(MODE, p.l2_policy_x, p.l2_policy_t);
   // the multi-block variants are instantiated for the fp32 W=32 vector path only
   if constexpr (std::is_same<T, float>::value && W == 32 && VEC) {
-    const int v = pipe_variant(MODE);
+    const int v = pipe_variant(MODE, p.K / W);
     if (v == 2) return launch_bfly_pipe<T, W, VEC, MODE, 2>(p, st);
     if (v == 3) return launch_bfly_pipe<T, W, VEC, MODE, 3>(p, st);
     if (v == 4) return launch_bfly_pipe<T, W, VEC, MODE, 4>(p, st);
+    if (v == 5) return launch_bfly_pipe<T, W, VEC, MODE, 5>(p, st);
+    if (v == 6) return launch_bfly_pipe<T, W, VEC, MODE, 6>(p, st);
   }
   return launch_bfly_pipe<T, W, VEC, MODE, 1>(p, st);
 }

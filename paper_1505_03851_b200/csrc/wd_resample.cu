@@ -9,9 +9,8 @@
 // Statistical (not bitwise) parity: the reference draws its Gammas from
 // numpy's PCG64 stream, which has no device equivalent.  Here every Gamma
 // is drawn from a counter-based stream keyed by (seed, row, topic, attempt)
-// -- the SplitMix64 finalizer over a Weyl counter (the same mixer the
-// reference's rng.py uses), 64 bits per evaluation -- so the result is
-// independent of launch geometry and of the number of GPUs.  Marsaglia-Tsang
+// -- a 32-bit integer hash of the counter -- so the result is independent of
+// launch geometry and of the number of GPUs.  Marsaglia-Tsang
 // (shape < 1 boosted by U^(1/a)) is evaluated in LOG space, so the tiny
 // Gammas of alpha = 0.1 / beta = 0.01 shapes never underflow before
 // normalisation.  Reductions use a fixed order, so a given (seed, counts)
@@ -29,31 +28,40 @@ namespace wd {
 int device_sm_count();
 void set_last_cuda_error(cudaError_t e);
 
-// four 32-bit words for attempt `ctr` of Gamma (row, k): two SplitMix64
-// finalizer evaluations of a Weyl sequence keyed by (seed, row, k)
+// Four 32-bit words for attempt `ctr` of Gamma (row, k): a 32-bit integer
+// hash (lowbias32 finalizer) of a counter built from a per-row key, the topic
+// and the attempt -- single-instruction 32-bit multiplies, ~7 instructions
+// per word (the 64-bit SplitMix/Philox alternatives cost 3-4x more here).
 struct Rand4 {
   uint32_t x, y, z, w;
 };
-__device__ __forceinline__ uint64_t gamma_key(uint64_t seed, uint64_t row, uint32_t k) {
-  return mix64(mix64(seed ^ row) ^ (uint64_t)k);
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
 }
-__device__ __forceinline__ Rand4 rand4(uint64_t key, uint32_t ctr) {
-  const uint64_t a = fin64(key + (2ull * ctr + 1ull) * GAMMA);
-  const uint64_t b = fin64(key + (2ull * ctr + 2ull) * GAMMA);
-  return {(uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32)};
+__device__ __forceinline__ uint32_t row_key(uint64_t seed, uint64_t row) {
+  return hash32((uint32_t)seed ^ hash32((uint32_t)row ^ hash32((uint32_t)(row >> 32) ^ (uint32_t)(seed >> 32))));
+}
+__device__ __forceinline__ Rand4 rand4(uint32_t rkey, uint32_t k, uint32_t ctr) {
+  const uint32_t base = hash32(rkey ^ (k * 0x9E3779B9u)) + ctr * 0x632BE5ABu;
+  return {hash32(base), hash32(base + 0x85EBCA6Bu), hash32(base + 0xC2B2AE35u), hash32(base + 0x27D4EB2Fu)};
 }
 
 // uniform in (0, 1): 24-bit mantissa, never 0
 __device__ __forceinline__ float u01(uint32_t x) { return ((float)(x >> 8) + 0.5f) * 0x1p-24f; }
 
 // One Marsaglia-Tsang attempt (2000) for log Gamma(a, 1) from the counter
-// block (key(seed, row, topic), ctr); shapes a < 1 use the boost Gamma(a) = Gamma(a + 1)
+// block (row key, topic, attempt); shapes a < 1 use the boost Gamma(a) = Gamma(a + 1)
 // * U^(1/a) (numpy's construction) with U taken from the same block -- its
 // acceptance depends only on the other three words, so U stays independent.
 // Evaluated in LOG space so alpha = 0.1 / beta = 0.01 shapes never underflow.
 // SFU approximations (__logf, __cosf, rsqrtf): statistical, not bitwise.
-__device__ __forceinline__ bool log_gamma_attempt(float a, uint64_t key, uint32_t ctr, float& out) {
-  const Rand4 r = rand4(key, ctr);
+__device__ __forceinline__ bool log_gamma_attempt(float a, uint32_t rkey, uint32_t k, uint32_t ctr, float& out) {
+  const Rand4 r = rand4(rkey, k, ctr);
   float boost = 0.f;
   if (a < 1.f) {
     boost = __logf(u01(r.w)) * __frcp_rn(a);
@@ -114,16 +122,14 @@ __global__ void __launch_bounds__(256) theta_kernel(const int32_t* __restrict__ 
     // per-lane progress: a rejection costs that lane one more attempt instead
     // of stalling the whole warp at every topic (divergence only at the tail)
     uint32_t ctr = 0;
-    const uint64_t rkey = mix64(seed ^ row);
-    uint64_t key = mix64(rkey ^ (uint64_t)lane);
+    const uint32_t rkey = row_key(seed, row);
     for (int k = lane; k < K;) {
       float v;
-      if (log_gamma_attempt(alpha + (float)hist[k], key, ctr, v)) {
+      if (log_gamma_attempt(alpha + (float)hist[k], rkey, (uint32_t)k, ctr, v)) {
         lg[k] = v;
         mx = fmaxf(mx, v);
         k += 32;
         ctr = 0;
-        key = mix64(rkey ^ (uint64_t)k);
       } else {
         ++ctr;
       }
@@ -160,15 +166,15 @@ __global__ void __launch_bounds__(kPhiThreads) phi_pass(int pass, const int32_t*
     const float cs = pass == 0 ? 0.f : colstat[k];
     if (pass == 0) {
       uint32_t ctr = 0;
-      uint64_t key = gamma_key(seed, (uint64_t)v0, (uint32_t)k);
+      uint32_t rkey = row_key(seed, (uint64_t)v0);
       for (int64_t v = v0; v < v1;) {
         float lgv;
-        if (log_gamma_attempt(beta + (float)wt[v * (int64_t)K + k], key, ctr, lgv)) {
+        if (log_gamma_attempt(beta + (float)wt[v * (int64_t)K + k], rkey, (uint32_t)k, ctr, lgv)) {
           phi[v * ld + k] = (T)lgv;
           acc = fmaxf(acc, lgv);
           ++v;
           ctr = 0;
-          key = gamma_key(seed, (uint64_t)v, (uint32_t)k);
+          rkey = row_key(seed, (uint64_t)v);
         } else {
           ++ctr;
         }
