@@ -135,9 +135,14 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ corpus
 def make_shard(torch, rank, args, device):
+    """One GPU's document shard; padded with empty documents to a multiple of
+    32 (Corpus.padded, lda.py:56-63) so shards stay 32-aligned."""
     g = torch.Generator(device=device).manual_seed(args.seed * 1000 + rank)
     M = args.docs_per_gpu
     lengths = torch.poisson(torch.full((M,), args.mean_len, device=device), generator=g).clamp_(min=1).long()
+    if M % 32:
+        lengths = torch.cat([lengths, torch.zeros(32 - M % 32, dtype=torch.long, device=device)])
+        M = lengths.numel()
     off = torch.zeros(M + 1, dtype=torch.int64, device=device)
     off[1:] = torch.cumsum(lengths, 0)
     T = int(off[-1].item())
@@ -251,7 +256,7 @@ def main():
     peak, peak_src = load_peaks()
 
     off, words = make_shard(torch, rank, args, dev)
-    doc_base = rank * args.docs_per_gpu
+    doc_base = rank * (off.numel() - 1)
     dcorpus = wd.DeviceCorpus.from_csr(off, words, doc_base=doc_base, vocab_size=V)
     n_tok = dcorpus.n_tokens
     lda = DeviceLDA(dcorpus, K, V, lanes=32, seed=args.seed, process_group=pg)

@@ -359,3 +359,65 @@ def test_vocab_tiled_draw_identical(kernel):
                           key_rule=O.KEY_POSITION if kernel == "basic" else O.KEY_MASTER)
     z = wd.draw_z_device(kernel, dc, th, ph, wd.SeededStops(5), 32, tiles=tiles).cpu().numpy()
     np.testing.assert_array_equal(z, exp)
+
+
+def test_full_size_lda_k1024_sampled_tokens():
+    """The bench shape (BASELINE configs[3] per GPU: 1M documents, Poisson(200)
+    lengths, V=40k, K=1024, vocabulary-tiled): 4096 randomly chosen tokens are
+    re-drawn one by one by the oracle from the same theta/phi rows, u and
+    master-index key, and must match bit-for-bit; the fused word-topic counts
+    must sum to the token count."""
+    from paper_1505_03851_b200.device_lda import DeviceLDA
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    M, V, K = 1_000_000, 40_000, 1024
+    lengths = torch.poisson(torch.full((M,), 200.0, device="cuda"), generator=g).clamp_(min=1).long()
+    off = torch.zeros(M + 1, dtype=torch.int64, device="cuda")
+    off[1:] = torch.cumsum(lengths, 0)
+    T = int(off[-1])
+    words = torch.randint(0, V, (T,), generator=g, device="cuda", dtype=torch.int32)
+    dc = wd.DeviceCorpus.from_csr(off, words)
+    lda = DeviceLDA(dc, K, V, seed=11)
+    lda.init_uniform()
+    assert lda.tiles is not None and lda.tiles.n_tiles == 4
+    lda.draw(0)
+    lda.check_errors()
+    assert int(lda.word_topic.sum()) == T
+    z = lda.z
+    offh = off.cpu().numpy()
+    Nh = np.diff(offh)
+    rng = np.random.default_rng(0)
+    toks = np.sort(rng.choice(T, 4096, replace=False))
+    docs = np.searchsorted(offh, toks, side="right") - 1
+    seed = wd.derive_seed(11, 1, 0)
+    th = lda.theta[torch.from_numpy(docs).cuda()].cpu().numpy()
+    wt = words[torch.from_numpy(toks).cuda()].long()
+    ph = lda.phi[wt].cpu().numpy()
+    zs = z[torch.from_numpy(toks).cuda()].cpu().numpy()
+    gmax = Nh.reshape(-1, 32).max(axis=1)
+    for j, (t, m) in enumerate(zip(toks, docs)):
+        i = t - offh[m]
+        key = gmax[m // 32] - 1 if i == Nh[m] - 1 else i
+        u = O.units(seed, [m], [key])[0]
+        a = (th[j] * ph[j]).astype(np.float32)
+        idx, _, _ = O.draw_one(a, 32, int(m % 32), u=u)
+        assert idx == zs[j], (t, m, i)
+
+
+@pytest.mark.parametrize("K,W,dtype", [(4096, 32, np.float32), (200, 32, np.float32), (640, 8, np.float32),
+                                       (320, 64, np.float32), (1024, 32, np.float64)])
+def test_lda_large_k_and_lanes_tiled_vs_oracle(K, W, dtype):
+    """K up to 4096 (BASELINE configs[4] row length), other lane counts and
+    float64, drawn through vocabulary tiles, against the oracle."""
+    gen = np.random.default_rng(K + W)
+    M, V = 256, 300
+    N, off, words = _random_corpus(gen, M, V, 20)
+    theta = gen.dirichlet(np.full(K, 0.1), size=M).astype(dtype)
+    phi = gen.uniform(0.01, 1, size=(V, K)).astype(dtype)
+    dc = wd.DeviceCorpus.from_csr(off, words.astype(np.int32))
+    tiles = dc.vocab_tiles(64)
+    seed = 77
+    z = wd.draw_z_device("butterfly", dc, _cuda(theta), _cuda(phi), wd.SeededStops(seed), W, tiles=tiles).cpu().numpy()
+    exp, err = O.draw_z_csr(theta, phi, off, words, W=W, seed=seed, threads=8)
+    assert err is None
+    np.testing.assert_array_equal(z, exp)

@@ -8,7 +8,9 @@ import paper_1505_03851_b200 as wd  # noqa: E402
 from paper_1505_03851_b200.device_lda import DeviceLDA  # noqa: E402
 
 g = torch.Generator(device="cuda").manual_seed(0)
-M, V, K = int(sys.argv[1]) if len(sys.argv) > 1 else 200000, 40000, 1024
+M, V = int(sys.argv[1]) if len(sys.argv) > 1 else 200000, 40000
+K = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+MBS = [int(x) for x in (sys.argv[3] if len(sys.argv) > 3 else "10,16,20,27,32,41").split(",")]
 lengths = torch.poisson(torch.full((M,), 200.0, device="cuda"), generator=g).clamp_(min=1).long()
 off = torch.zeros(M + 1, dtype=torch.int64, device="cuda")
 off[1:] = torch.cumsum(lengths, 0)
@@ -30,7 +32,7 @@ def timeit(f, n=5):
     return a.elapsed_time(c) / n
 
 
-for mb in (10, 16, 20, 27, 32, 41):
+for mb in MBS:
     lda = DeviceLDA(dc, K, V, vocab_tile_bytes=mb << 20)
     lda.init_uniform()
     ms = timeit(lambda: lda.draw(0))
