@@ -68,8 +68,9 @@ def build(force: bool = False, ptxas_verbose: bool = False, verbose: bool = True
     def compile_one(src):
         obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
         f = list(flags)
-        if src in STATISTICAL_SOURCES:  # no bitwise contract: let FMA contraction in
+        if src in STATISTICAL_SOURCES:  # no bitwise contract: FMA contraction, flush-to-zero
             f[f.index("-fmad=false")] = "-fmad=true"
+            f.append("-ftz=true")
         cmd = [cc, *f, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -59,12 +59,13 @@ __device__ __forceinline__ float u01(uint32_t x) { return ((float)(x >> 8) + 0.5
 // * U^(1/a) (numpy's construction) with U taken from the same block -- its
 // acceptance depends only on the other three words, so U stays independent.
 // Evaluated in LOG space so alpha = 0.1 / beta = 0.01 shapes never underflow.
-// SFU approximations (__logf, __cosf, rsqrtf): statistical, not bitwise.
+// SFU approximations (__logf, __cosf, rsqrtf, __fdividef; this file is
+// compiled with FMA contraction and flush-to-zero): statistical, not bitwise.
 __device__ __forceinline__ bool log_gamma_attempt(float a, uint32_t rkey, uint32_t k, uint32_t ctr, float& out) {
   const Rand4 r = rand4(rkey, k, ctr);
   float boost = 0.f;
   if (a < 1.f) {
-    boost = __logf(u01(r.w)) * __frcp_rn(a);
+    boost = __fdividef(__logf(u01(r.w)), a);
     a += 1.f;
   }
   const float d = a - (1.f / 3.f);
