@@ -72,14 +72,24 @@ class DeviceLDA:
         self.phi.uniform_(low, high, generator=g)
 
     def init_from_assignments(self, t: int = -1):
-        """init_assignments + resample at iteration -1 (lda.py:264-265), device RNG."""
+        """Uniform random initial topics + resample at iteration -1
+        (lda.py:264-265).  The initial topic of token (doc m, position i) is
+        floor(K * units_for(derive_seed(seed, 0), m, i)) with GLOBAL doc ids,
+        so any sharding of the corpus gives the same start."""
         torch = self.torch
-        g = torch.Generator(device=self.device).manual_seed(int(derive_seed(self.seed, 0, self.corpus.doc_base)))
-        self.z.random_(0, self.K, generator=g)
+        c = self.corpus
+        if c.n_tokens:
+            pos = torch.arange(c.n_tokens, dtype=torch.int64, device=self.device) - c.offsets[c.token_doc.long()]
+            gdoc = c.token_doc.long() + c.doc_base
+            u = torch.empty(c.n_tokens, dtype=torch.float64, device=self.device)
+            L = _lib.load()
+            _lib.check(L.wd_units(derive_seed(self.seed, 0), 2, gdoc.data_ptr(), pos.data_ptr(), c.n_tokens,
+                                  u.data_ptr(), _lib.stream_handle()), "wd_units")
+            self.z.copy_((u * self.K).to(torch.int32).clamp_(max=self.K - 1))
         self.word_topic.zero_()
         L = _lib.load()
-        _lib.check(L.wd_topic_counts(self.corpus.words.data_ptr(), None, self.z.data_ptr(), self.corpus.n_tokens,
-                                     self.K, None, self.word_topic.data_ptr(), _lib.stream_handle()), "wd_topic_counts")
+        _lib.check(L.wd_topic_counts(c.words.data_ptr(), None, self.z.data_ptr(), c.n_tokens, self.K, None,
+                                     self.word_topic.data_ptr(), _lib.stream_handle()), "wd_topic_counts")
         if self.pg is not None:
             torch.distributed.all_reduce(self.word_topic, group=self.pg)
         self.resample(t)

@@ -1,0 +1,76 @@
+"""Multi-rank DeviceLDA on ONE GPU (gloo backend, both ranks on cuda:0): a
+2-shard run must reproduce the single-process run exactly -- z, the
+all-reduced word-topic counts, phi and theta -- because shards are
+32-aligned, keys use global document ids and every Gamma stream is keyed by
+(seed, global row, topic).  This exercises the same code path bench.py runs
+over NCCL on N GPUs (only the all-reduce transport differs)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _problem():
+    gen = np.random.default_rng(12)
+    M, V, K = 512, 700, 96
+    N = np.maximum(gen.poisson(40, size=M), 0)
+    off = np.concatenate([[0], np.cumsum(N)]).astype(np.int64)
+    words = gen.integers(0, V, size=int(off[-1])).astype(np.int32)
+    return M, V, K, N, off, words
+
+
+def _run(rank, world, port, out_dir, iters):
+    import paper_1505_03851_b200 as wd
+    from paper_1505_03851_b200.device_lda import DeviceLDA
+    from paper_1505_03851_b200.sharding import shard_csr, shard_ranges
+
+    torch.cuda.set_device(0)
+    M, V, K, N, off, words = _problem()
+    pg = None
+    lo, hi = 0, M
+    if world > 1:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        pg = dist.group.WORLD
+        lo, hi = shard_ranges(N, world)[rank]
+    soff, swords = shard_csr(off, words, lo, hi)
+    dc = wd.DeviceCorpus.from_csr(soff, swords, doc_base=lo)
+    lda = DeviceLDA(dc, K, V, seed=5, process_group=pg, vocab_tile_bytes=64 * K * 4)
+    lda.init_from_assignments()
+    for t in range(iters):
+        lda.iterate(t)
+    lda.check_errors()
+    ll = lda.log_likelihood()
+    np.savez(os.path.join(out_dir, f"r{world}_{rank}.npz"), z=lda.z.cpu().numpy(), theta=lda.theta.cpu().numpy(),
+             phi=lda.phi.cpu().numpy(), wt=lda.word_topic.cpu().numpy(), ll=np.array(ll))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_reproduce_one(tmp_path):
+    iters = 3
+    _run(0, 1, 0, str(tmp_path), iters)
+    mp.start_processes(_run, args=(2, _free_port(), str(tmp_path), iters), nprocs=2, join=True,
+                       start_method="spawn")
+    one = np.load(tmp_path / "r1_0.npz")
+    parts = [np.load(tmp_path / f"r2_{r}.npz") for r in range(2)]
+    np.testing.assert_array_equal(np.concatenate([p["z"] for p in parts]), one["z"])
+    np.testing.assert_array_equal(np.concatenate([p["theta"] for p in parts]), one["theta"])
+    for p in parts:
+        np.testing.assert_array_equal(p["wt"], one["wt"])
+        np.testing.assert_array_equal(p["phi"], one["phi"])
+        assert abs(float(p["ll"]) - float(one["ll"])) <= 1e-9 * abs(float(one["ll"]))
