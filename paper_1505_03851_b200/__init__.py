@@ -28,11 +28,13 @@ from .lda import (
     gibbs_iterate,
     init_assignments,
     load_corpus,
+    load_corpus_npz,
     log_likelihood,
     modal_topics,
     resample_params,
     run_gibbs,
     save_corpus,
+    save_corpus_npz,
     topic_counts,
 )
 from .rng import derive_seed, mix64, unit_for, units_for

@@ -120,6 +120,16 @@ def test_corpus_file_roundtrip(tmp_path):
         wd.load_corpus(p)
 
 
+def test_corpus_npz_roundtrip(tmp_path):
+    c = wd.Corpus(vocab_size=9, lengths=np.array([3, 0, 1]), words=[np.array([1, 8, 2]), np.zeros(0), np.array([0])])
+    p = tmp_path / "c.npz"
+    wd.save_corpus_npz(c.padded(4), p)
+    d = wd.load_corpus_npz(p)
+    assert d.vocab_size == 9 and d.padding == 1 and d.n_docs == 4
+    np.testing.assert_array_equal(d.lengths, [3, 0, 1, 0])
+    np.testing.assert_array_equal(d.words[0], [1, 8, 2])
+
+
 def test_init_assignments_matches_reference_stream():
     c = wd.Corpus(vocab_size=5, lengths=np.array([4, 0, 2]), words=[np.zeros(4), np.zeros(0), np.zeros(2)])
     z = wd.init_assignments(c, 7, 11)
