@@ -41,6 +41,9 @@ enum { MODE_LDA = 0, MODE_ROWS = 1 };
 #ifndef WD_LDA_MIN_BLOCKS
 #define WD_LDA_MIN_BLOCKS 6
 #endif
+#ifndef WD_LDA_MIN_BLOCKS_COARSE  // K > 32 * W: the group recompute needs more registers
+#define WD_LDA_MIN_BLOCKS_COARSE 4
+#endif
 
 template <typename T> struct DrawParams {
   const T* theta;  // LDA: doc rows (ld_theta); ROWS: unused
@@ -303,6 +306,15 @@ __device__ __forceinline__ T block_total_nd0(const RowSet<T, Geo<W>::L>& P,
   return xreduce<T, L>(q, s);
 }
 
+// Running sums are kept for every G-th block only (G = ceil(nb / 32)), so a
+// warp's S array stays <= 32 entries per lane for any K; the exact S_b of
+// the selected group are recomputed after the search (same IEEE operations).
+template <typename T>
+__device__ __forceinline__ void store_s(T* __restrict__ S, int b, int nb, int G, int lane, T v) {
+  if (G == 1) S[b * 32 + lane] = v;
+  else if ((b + 1) % G == 0 || b == nb - 1) S[(b / G) * 32 + lane] = v;
+}
+
 // Pass 1 over all blocks: running block sums S_b of the own row
 // (sequential over blocks, kernels.py:221-223).  Memory-level parallelism:
 //   PIPE = 1  one block's loads in flight, then its arithmetic;
@@ -313,7 +325,7 @@ __device__ __forceinline__ T bfly_blocks(const RowSet<T, Geo<W>::L>& prow,
                                          const RowSet<T, (Geo<W>::L < 2 ? 2 : Geo<W>::L)>& trow,
                                          const bool (&rvalid)[Geo<W>::L], int nb, int s, T acc,
                                          T* __restrict__ S, int lane, uint64_t px, uint64_t pt,
-                                         uint32_t opaque_zero, uint32_t dsel, bool raw) {
+                                         uint32_t opaque_zero, uint32_t dsel, bool raw, int G) {
   // raw: store the block totals T_b themselves (the running sums are formed
   // after the remnant prefix is known); else S_b = S_{b-1} + T_b directly
   using R = BlockRegs<T, W, VEC, MODE, ND>;
@@ -321,7 +333,7 @@ __device__ __forceinline__ T bfly_blocks(const RowSet<T, Geo<W>::L>& prow,
     for (int b = 0; b < nb; ++b) {
       const T t = block_total_nd0<T, W, VEC>(prow, trow, (int64_t)b * W, rvalid, s, px, pt);
       acc = raw ? t : add_rn(acc, t);
-      S[b * 32 + lane] = acc;
+      store_s(S, b, nb, G, lane, acc);
     }
   } else if (PIPE == 1 || PIPE == 4) {
     for (int b = 0; b < nb; ++b) {
@@ -330,7 +342,7 @@ __device__ __forceinline__ T bfly_blocks(const RowSet<T, Geo<W>::L>& prow,
       if (PIPE == 4) cur.join(opaque_zero);
       const T t = cur.reduce(rvalid, s, dsel);
       acc = raw ? t : add_rn(acc, t);
-      S[b * 32 + lane] = acc;
+      store_s(S, b, nb, G, lane, acc);
     }
   } else if (PIPE == 2) {
     R cur;
@@ -340,7 +352,7 @@ __device__ __forceinline__ T bfly_blocks(const RowSet<T, Geo<W>::L>& prow,
       if (b + 1 < nb) nxt.load(prow, trow, (int64_t)(b + 1) * W, px, pt);
       const T t = cur.reduce(rvalid, s, dsel);
       acc = raw ? t : add_rn(acc, t);
-      S[b * 32 + lane] = acc;
+      store_s(S, b, nb, G, lane, acc);
       cur = nxt;
     }
   } else {
@@ -351,17 +363,17 @@ __device__ __forceinline__ T bfly_blocks(const RowSet<T, Geo<W>::L>& prow,
       c1.load(prow, trow, (int64_t)(b + 1) * W, px, pt);
       const T t0 = c0.reduce(rvalid, s, dsel);
       acc = raw ? t0 : add_rn(acc, t0);
-      S[b * 32 + lane] = acc;
+      store_s(S, b, nb, G, lane, acc);
       const T t1 = c1.reduce(rvalid, s, dsel);
       acc = raw ? t1 : add_rn(acc, t1);
-      S[(b + 1) * 32 + lane] = acc;
+      store_s(S, b + 1, nb, G, lane, acc);
     }
     if (b < nb) {
       R c0;
       c0.load(prow, trow, (int64_t)b * W, px, pt);
       const T t0 = c0.reduce(rvalid, s, dsel);
       acc = raw ? t0 : add_rn(acc, t0);
-      S[b * 32 + lane] = acc;
+      store_s(S, b, nb, G, lane, acc);
     }
   }
   return acc;
@@ -386,7 +398,7 @@ __device__ __forceinline__ T bfly_blocks_ring(const RowSet<T, Geo<W>::L>& prow,
                                               const RowSet<T, (Geo<W>::L < 2 ? 2 : Geo<W>::L)>& trow,
                                               const bool (&rvalid)[Geo<W>::L], int nb, int s, T acc,
                                               T* __restrict__ S, int lane, uint32_t dsel, bool raw,
-                                              char* __restrict__ ring) {
+                                              char* __restrict__ ring, int G) {
   static_assert(sizeof(T) * Geo<W>::E == 16, "ring path needs 16-byte segments");
   constexpr int L = Geo<W>::L;
   constexpr int NT = MODE == MODE_LDA ? ND : 0;
@@ -424,7 +436,7 @@ __device__ __forceinline__ T bfly_blocks_ring(const RowSet<T, Geo<W>::L>& prow,
     }
     const T t = cur.reduce(rvalid, s, dsel);
     acc = raw ? t : add_rn(acc, t);
-    S[b * 32 + lane] = acc;
+    store_s(S, b, nb, G, lane, acc);
   }
   cp_async_wait_n<0>();
   return acc;
@@ -450,28 +462,34 @@ template <typename T> struct Walk<T, 0> {
   static __device__ __forceinline__ void run(T*, T&, T&, T, int, int&) {}
 };
 
-template <typename T, int W, bool VEC, int MODE, int PIPE>
+template <typename T, int W, bool VEC, int MODE, int PIPE, bool COARSE>
 __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
-                                             ? (PIPE == 2 ? 4 : (MODE == MODE_LDA ? WD_LDA_MIN_BLOCKS : 8))
+                                             ? (PIPE == 2 ? 4
+                                                          : (MODE == MODE_LDA ? (COARSE ? WD_LDA_MIN_BLOCKS_COARSE
+                                                                                        : WD_LDA_MIN_BLOCKS)
+                                                                              : 8))
                                              : 1)
     bfly_kernel(DrawParams<T> p) {
-  using G = Geo<W>;
-  constexpr int E = G::E, L = G::L, R = G::R;
+  using GW = Geo<W>;
+  constexpr int E = GW::E, L = GW::L, R = GW::R;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int K = p.K;
   const int nb = K / W, rem = K % W;
+  // coarse running sums beyond 32 blocks (COARSE instantiation only)
+  const int G = COARSE ? (nb > 32 ? (nb + 31) / 32 : 1) : 1;
+  const int nbc = nb > 0 ? (nb + G - 1) / G : 1;
   const int wpb_i = blockDim.x >> 5;
-  T* S = reinterpret_cast<T*>(smem_raw) + (size_t)wib * (size_t)(nb > 0 ? nb : 1) * 32;
+  T* S = reinterpret_cast<T*>(smem_raw) + (size_t)wib * (size_t)nbc * 32;
   // remnant tile [32 rows][TS] per warp (after every warp's S).  Vector path:
   // stride W + 4 keeps rows 16-byte aligned and the 128-bit segment stores /
   // row scans conflict-free; scalar path: odd stride W + 1.
   constexpr int TS = VEC ? W + 4 : W + 1;
-  T* RT = reinterpret_cast<T*>(smem_raw) + (size_t)wpb_i * (size_t)(nb > 0 ? nb : 1) * 32 + (size_t)wib * 32 * TS;
+  T* RT = reinterpret_cast<T*>(smem_raw) + (size_t)wpb_i * (size_t)nbc * 32 + (size_t)wib * 32 * TS;
   // cp.async ring (PIPE 5/6), after every warp's S and remnant tile
   constexpr bool RING = PIPE >= 5;
-  char* ring = reinterpret_cast<char*>(reinterpret_cast<T*>(smem_raw) + (size_t)wpb_i * (size_t)(nb > 0 ? nb : 1) * 32 +
+  char* ring = reinterpret_cast<char*>(reinterpret_cast<T*>(smem_raw) + (size_t)wpb_i * (size_t)nbc * 32 +
                                        (size_t)wpb_i * 32 * TS) +
                (size_t)wib * RingDepth<PIPE>::NS * RingStage<W>::BYTES;
   const int s = lane % L;
@@ -526,7 +544,9 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
     // the block loop then stores raw block totals and the running sums are
     // formed once the remnant prefix is known (same IEEE additions).
     T acc = T(0);
-    const bool async_rem = VEC && rem > 0 && rem % E == 0 && (E * sizeof(T)) % 16 == 0;
+    const bool async_rem = VEC && rem > 0 && rem % E == 0 && (E * sizeof(T)) % 16 == 0 && G == 1;
+    const bool raw = async_rem;  // block totals stored raw, running sums formed after the loop
+    T prem = T(0);
     if (async_rem) {
 #pragma unroll
       for (int kk = 0; kk < L; ++kk) {
@@ -567,6 +587,9 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
           }
         }
       }
+      __syncwarp();
+      for (int t = 0; t < rem; ++t) prem = add_rn(prem, RT[own * TS + t]);  // sequential
+      acc = prem;
     }
     // theta rows the chunk needs: one document (ND=1), two (ND=2: the rows of
     // the second one are flagged in dsel), or more (ND=0: per-row loads).
@@ -595,30 +618,29 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
     if constexpr (RING) {
       if (MODE == MODE_ROWS || nd == 1)
         acc = bfly_blocks_ring<T, W, MODE, 1, RingDepth<PIPE>::NS>(prow, trow_nd, rvalid, nb, s, acc, S, lane, 0u,
-                                                                   rem > 0, ring);
+                                                                   raw, ring, G);
       else if (nd == 2)
         acc = bfly_blocks_ring<T, W, MODE, 2, RingDepth<PIPE>::NS>(prow, trow_nd, rvalid, nb, s, acc, S, lane, dsel,
-                                                                   rem > 0, ring);
+                                                                   raw, ring, G);
       else  // >2 documents: per-row theta segments, register path
         acc = bfly_blocks<T, W, VEC, MODE, 0, 1>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
-                                                 p.opaque_zero, 0u, rem > 0);
+                                                 p.opaque_zero, 0u, raw, G);
     } else if constexpr (MODE == MODE_ROWS) {
       acc = bfly_blocks<T, W, VEC, MODE, 1, PIPE>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
-                                                  p.opaque_zero, 0u, rem > 0);
+                                                  p.opaque_zero, 0u, raw, G);
     } else {
       if (nd == 1)
         acc = bfly_blocks<T, W, VEC, MODE, 1, PIPE>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
-                                                    p.opaque_zero, 0u, rem > 0);
+                                                    p.opaque_zero, 0u, raw, G);
       else if (nd == 2)
         acc = bfly_blocks<T, W, VEC, MODE, 2, PIPE>(prow, trow_nd, rvalid, nb, s, acc, S, lane, pol_x, pol_t,
-                                                    p.opaque_zero, dsel, rem > 0);
+                                                    p.opaque_zero, dsel, raw, G);
       else  // >2 documents: per-row theta segments
         acc = bfly_blocks<T, W, VEC, MODE, 0, (PIPE != 4 ? 1 : PIPE)>(prow, trow_nd, rvalid, nb, s, acc, S, lane,
-                                                                      pol_x, pol_t, p.opaque_zero, 0u, rem > 0);
+                                                                      pol_x, pol_t, p.opaque_zero, 0u, raw, G);
     }
-    T prem = T(0);
-    if (rem > 0) {
-      if (async_rem) cp_async_wait_all();
+    if (raw) {
+      cp_async_wait_all();
       __syncwarp();
       // sequential remnant prefix of the own row (products formed here on the
       // asynchronous path, already in the tile on the synchronous one)
@@ -635,8 +657,6 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
 #pragma unroll
           for (int e = 0; e < E; ++e) prem = add_rn(prem, a[e]);
         }
-      } else {
-        for (int t = 0; t < rem; ++t) prem = add_rn(prem, RT[own * TS + t]);
       }
       acc = prem;
       for (int b = 0; b < nb; ++b) {  // S_b = S_{b-1} + T_b from the raw totals
@@ -655,20 +675,14 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
       token_keys<T, MODE>(p, own_tok, own_doc, W, ka, kb, ekey, r, zidx);
       const T stop = make_stop<T>(p, zidx, total, ka, kb, MODE == MODE_ROWS);
       if (!(total > T(0))) atomicMin(p.err, ekey);
-      // block bisection over S (kernels.py:337-346)
-      int j = 0, k = nb - 1;
-      while (j < k) {
-        const int mid = (j + k) >> 1;
-        if (stop < S[mid * 32 + lane]) k = mid; else j = mid + 1;
-      }
-      const int64_t bb = (int64_t)rem + (int64_t)j * W;
-      const T prev = bb > 0 ? (j > 0 ? S[(j - 1) * 32 + lane] : prem) : T(0);
-      const bool fallback = bb > 0 && stop < prev && total > T(0);
-      int result = 0;
-      if (nb > 0 && !fallback) {
-        // rebuild the selected block's products (own row) and walk it; the
-        // loads go in two halves to bound live registers
-        T cur[W];
+      // block bisection over S (kernels.py:337-346): the first block whose
+      // running sum exceeds stop (S is nondecreasing, so any search that finds
+      // that block is the reference's bisection)
+      T cur[W];
+      bool have_cur = false;
+      int j;
+      T prev, high;
+      auto load_block = [&](int64_t base) {  // own row's products of one block
         constexpr int NG = W / E;
         constexpr int HG = NG >= 4 ? NG / 2 : NG;
 #pragma unroll
@@ -676,10 +690,10 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
 #pragma unroll
           for (int g = h; g < h + HG; ++g) {
             Seg<T, E, VEC> x;
-            x.load(pown + bb + g * E);
+            x.load(pown + base + g * E);
             if (MODE == MODE_LDA) {
               Seg<T, E, VEC> th;
-              th.load(town + bb + g * E);
+              th.load(town + base + g * E);
 #pragma unroll
               for (int e = 0; e < E; ++e) cur[g * E + e] = mul_rn(th.v[e], x.v[e]);
             } else {
@@ -688,7 +702,46 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
             }
           }
         }
-        T low = prev, high = S[j * 32 + lane];
+      };
+      {
+        int lo2 = 0, hi2 = nbc - 1;
+        while (lo2 < hi2) {
+          const int mid = (lo2 + hi2) >> 1;
+          if (stop < S[mid * 32 + lane]) hi2 = mid; else lo2 = mid + 1;
+        }
+        if (!COARSE || G == 1) {
+          j = lo2;
+          prev = j > 0 ? S[(j - 1) * 32 + lane] : prem;
+          high = nb > 0 ? S[j * 32 + lane] : T(0);
+        } else {
+          // recompute the selected group's block totals and running sums
+          T run = lo2 > 0 ? S[(lo2 - 1) * 32 + lane] : prem;
+          const int b0 = lo2 * G, b1 = min(b0 + G, nb);
+          j = b1 - 1;
+          prev = run;
+          high = run;
+          for (int bj = b0; bj < b1; ++bj) {
+            load_block((int64_t)rem + (int64_t)bj * W);
+            const T sb = add_rn(run, Tree<T, W>::sum(cur));
+            if (stop < sb || bj == b1 - 1) {
+              j = bj;
+              prev = run;
+              high = sb;
+              break;
+            }
+            run = sb;
+          }
+          have_cur = true;
+        }
+      }
+      const int64_t bb = (int64_t)rem + (int64_t)j * W;
+      if (bb == 0) prev = T(0);
+      const bool fallback = bb > 0 && stop < prev && total > T(0);
+      int result = 0;
+      if (nb > 0 && !fallback) {
+        // rebuild the selected block's products (own row) and walk it
+        if (!COARSE || !have_cur) load_block(bb);
+        T low = prev;
         int lo = 0;
         Walk<T, W / 2>::run(cur, low, high, stop, r, lo);
         result = (int)bb + lo;

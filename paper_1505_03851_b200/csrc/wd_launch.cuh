@@ -42,7 +42,9 @@ inline int occupancy_blocks(const void* fn, size_t smem, int threads = kThreads)
 template <typename T>
 inline size_t bfly_smem_per_warp(int W, int K, int mode, int pipe = 1) {
   int nb = K / W;
-  size_t b = (size_t)(nb > 0 ? nb : 1) * 32 * sizeof(T);
+  int G = nb > 32 ? (nb + 31) / 32 : 1;  // coarse running sums (bfly_kernel)
+  int nbc = nb > 0 ? (nb + G - 1) / G : 1;
+  size_t b = (size_t)nbc * 32 * sizeof(T);
   if (K % W || pipe >= 5) b += (size_t)32 * (W + 4) * sizeof(T);  // remnant tile (the ring sits after it)
   if (pipe >= 5) b += (size_t)(pipe == 6 ? 4 : 3) * ((W >= 4 ? W / 4 : 1) + 2) * 32 * 16;  // cp.async ring
   return b;
@@ -75,9 +77,9 @@ inline void l2_policies(int mode, int& px, int& pt) {
   pt = lt >= 0 ? lt : 0;
 }
 
-template <typename T, int W, bool VEC, int MODE, int PIPE>
-int launch_bfly_pipe(const DrawParams<T>& p, cudaStream_t st) {
-  const void* fn = (const void*)bfly_kernel<T, W, VEC, MODE, PIPE>;
+template <typename T, int W, bool VEC, int MODE, int PIPE, bool COARSE>
+int launch_bfly_pc(const DrawParams<T>& p, cudaStream_t st) {
+  const void* fn = (const void*)bfly_kernel<T, W, VEC, MODE, PIPE, COARSE>;
   const size_t per_warp = bfly_smem_per_warp<T>(W, p.K, MODE, PIPE);
   int wpb = kThreads / 32;  // fewer warps per CTA when the block sums are large
   while (wpb > 1 && (size_t)wpb * per_warp > 227 * 1024) wpb >>= 1;
@@ -91,10 +93,17 @@ int launch_bfly_pipe(const DrawParams<T>& p, cudaStream_t st) {
   int64_t cap = (int64_t)per_sm * device_sm_count();
   int grid = (int)(want < cap ? want : cap);
   if (grid <= 0) return WD_OK;
-  bfly_kernel<T, W, VEC, MODE, PIPE><<<grid, threads, smem, st>>>(p);
+  bfly_kernel<T, W, VEC, MODE, PIPE, COARSE><<<grid, threads, smem, st>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { set_last_cuda_error(e); return WD_ERR_CUDA; }
   return WD_OK;
+}
+
+// more than 32 blocks per row: the coarse-running-sum instantiation
+template <typename T, int W, bool VEC, int MODE, int PIPE>
+int launch_bfly_pipe(const DrawParams<T>& p, cudaStream_t st) {
+  if (p.K / W > 32) return launch_bfly_pc<T, W, VEC, MODE, PIPE, true>(p, st);
+  return launch_bfly_pc<T, W, VEC, MODE, PIPE, false>(p, st);
 }
 
 template <typename T, int W, bool VEC, int MODE>
