@@ -417,7 +417,7 @@ def main():
     # ------------------------------------------------------- CPU baseline
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        S_max = min(dcorpus.n_docs, 262144)
+        S_max = dcorpus.n_docs
         th = (torch.rand((S_max, K), generator=torch.Generator(device=dev).manual_seed(1), device=dev) * 0.9
               + 0.1).cpu().numpy()
         # synth_params-style positive theta/phi (bench.py:187-192 of the
