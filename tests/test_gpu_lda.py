@@ -109,3 +109,43 @@ def test_device_lda_improves_likelihood_and_recovers_planted_topics():
     from sklearn.metrics import adjusted_rand_score
 
     assert adjusted_rand_score(labels, modal) >= 0.9
+
+
+def test_device_lda_loglikelihood_matches_reference_chain():
+    """North-star acceptance: the throughput mode (device Dirichlet resample,
+    its own RNG) tracks the reference's chain (parity mode = the reference's
+    numpy resample, bit-identical to warpdraw.run_gibbs) to within 1e-3
+    relative log-likelihood after a fixed number of iterations (mean of the
+    last 10 of 40 iterations, BASELINE configs[0] corpus shape)."""
+    import os
+
+    from conftest import GOLDEN
+
+    g = np.load(os.path.join(GOLDEN, "cfg1.npz"))
+    N = g["N"]
+    off = np.concatenate([[0], np.cumsum(N)])
+    words = g["words"].astype(np.int64)
+    corpus = wd.Corpus(vocab_size=5000, lengths=N, words=[words[off[m]:off[m + 1]] for m in range(N.size)])
+    iters = 40
+    _, _, ll_ref = wd.run_gibbs(corpus, 64, iters, "butterfly", wd.WarpConfig(32, 4), 7, dtype=np.float32)
+    padded = corpus.padded(32)
+    poff, pwords = padded.csr()
+    lda = DeviceLDA(wd.DeviceCorpus.from_csr(poff, pwords), 64, 5000, seed=7)
+    lda.init_from_assignments()
+    ll_dev = []
+    for t in range(iters):
+        lda.iterate(t)
+        ll_dev.append(lda.log_likelihood())
+    lda.check_errors()
+    a, b = np.mean(ll_ref[-10:]), np.mean(ll_dev[-10:])
+    assert abs(a - b) / abs(a) < 1e-3, (a, b)
+
+
+def test_sampler_chi_square():
+    """Acceptance criterion 6 (test_acceptance.py:270-298): 1e6 draws from 19
+    random weights through the GPU butterfly sampler pass chi-square at 0.001."""
+    gen = np.random.default_rng(60)
+    weights = gen.uniform(0.05, 1.0, size=19)
+    draws = wd.sample_butterfly(weights, 1_000_000, seed=61)
+    stat, dof = wd.chi_square(np.bincount(draws, minlength=19), weights / weights.sum())
+    assert dof == 18 and stat < wd.chi_square_critical(18, 0.001)
