@@ -92,7 +92,13 @@ int wd_corpus_prepare(const int64_t* doc_offsets, int64_t n_docs, int64_t n_toke
                       int64_t doc_base, int lanes, int32_t* token_doc, int32_t* last_key,
                       void* stream);
 
-/* Scratch bytes wd_draw_z / wd_sample_rows need (0 for WD_BUTTERFLY). */
+/*
+ * Scratch bytes wd_draw_z / wd_sample_rows need.  WD_PREFIX: the per-lane
+ * prefix tables.  WD_BUTTERFLY: none is required; with at least this much,
+ * wd_sample_rows on ONE shared weight vector (ld = 0) builds the butterfly
+ * table once and answers every draw by search (bench.py:129-147), instead
+ * of re-reading the vector per draw -- same results either way.
+ */
 size_t wd_workspace_bytes(int variant, int dtype, int lanes, int32_t n_topics);
 
 /*
@@ -176,6 +182,29 @@ int wd_log_likelihood(int dtype, const void* theta, int64_t ld_theta, const void
                       const int32_t* words, const int32_t* token_doc, int64_t n_docs, int64_t n_tokens,
                       int64_t vocab_size, int32_t n_topics, double* out, void* workspace,
                       size_t workspace_bytes, void* stream);
+
+/*
+ * Sequential-stream samplers: the reference's SAMPLERS["binary"] and
+ * SAMPLERS["alias"] (bench.py:118-126), one shared weight vector, n draws
+ * taken in order from ONE xoshiro256** stream seeded by SplitMix64 from
+ * `seed` (rng.py:47-77; seed = derive_seed(user_seed, 4) resp. (…, 5)).
+ * Every thread starts at its own stream position through GF(2) jump
+ * matrices built on the device, so draw i equals the reference's i-th draw.
+ *   WD_STREAM_BINARY: stop = table[K-1] * u; smallest j with stop < table[j]
+ *     (sampling.py:55-92); table = float64 running sums (wd_prefix_f64).
+ *   WD_STREAM_ALIAS:  k = trunc(u1 * K); k if bits(u2) < thresh[k] else
+ *     alias[k] (sampling.py:134-138); thresh[k] = ceil(F[k] * 2^53) of the
+ *     exact Vose acceptance F[k] (sampling.py:101-131), so the 53-bit
+ *     comparison is exactly the reference's float-vs-Fraction one.
+ * Scratch: wd_stream_workspace_bytes(n) bytes.
+ */
+#define WD_STREAM_BINARY 0
+#define WD_STREAM_ALIAS 1
+int wd_prefix_f64(const double* weights, int64_t n_weights, double* table, void* stream);
+size_t wd_stream_workspace_bytes(int64_t n_draws);
+int wd_stream_draws(int method, const double* table, const uint64_t* thresh, const int32_t* alias,
+                    int64_t n_weights, uint64_t seed, int64_t n_draws, int32_t* out, void* workspace,
+                    size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -38,7 +38,17 @@ from .lda import (
     topic_counts,
 )
 from .rng import derive_seed, mix64, unit_for, units_for
-from .samplers import SAMPLERS, chi_square, chi_square_critical, sample_butterfly, sample_prefix, sample_rows
+from .samplers import (
+    SAMPLERS,
+    alias_table,
+    chi_square,
+    chi_square_critical,
+    sample_alias,
+    sample_binary,
+    sample_butterfly,
+    sample_prefix,
+    sample_rows,
+)
 from .sampling import AllZeroError, EmptyWeightsError
 from .warp import Trace, WarpConfig
 

@@ -20,6 +20,7 @@ WD_FLOAT32, WD_FLOAT64 = 0, 1
 WD_BUTTERFLY, WD_PREFIX = 0, 1
 WD_STOPS_SEEDED, WD_STOPS_UNITS, WD_STOPS_EXPLICIT, WD_STOPS_PHILOX = 0, 1, 2, 3
 WD_KEYS_MASTER, WD_KEYS_POSITION = 0, 1
+WD_STREAM_BINARY, WD_STREAM_ALIAS = 0, 1
 ERR_NONE = (1 << 64) - 1
 
 EXPORTS = (
@@ -36,6 +37,9 @@ EXPORTS = (
     "wd_resample_phi_workspace_bytes",
     "wd_resample_phi",
     "wd_log_likelihood",
+    "wd_prefix_f64",
+    "wd_stream_workspace_bytes",
+    "wd_stream_draws",
 )
 
 
@@ -78,6 +82,12 @@ def _declare(L):
     L.wd_resample_phi.argtypes = [i32, vp, i64, ctypes.c_int32, dbl, u64, vp, i64, vp, sz, vp]
     L.wd_log_likelihood.restype = i32
     L.wd_log_likelihood.argtypes = [i32, vp, i64, vp, i64, vp, vp, i64, i64, i64, ctypes.c_int32, vp, vp, sz, vp]
+    L.wd_prefix_f64.restype = i32
+    L.wd_prefix_f64.argtypes = [vp, i64, vp, vp]
+    L.wd_stream_workspace_bytes.restype = sz
+    L.wd_stream_workspace_bytes.argtypes = [i64]
+    L.wd_stream_draws.restype = i32
+    L.wd_stream_draws.argtypes = [i32, vp, vp, vp, i64, u64, i64, vp, vp, sz, vp]
 
 
 def load(path: str | None = None):

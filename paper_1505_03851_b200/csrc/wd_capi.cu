@@ -171,8 +171,11 @@ int wd_corpus_prepare(const int64_t* doc_offsets, int64_t n_docs, int64_t n_toke
 }
 
 size_t wd_workspace_bytes(int variant, int dtype, int lanes, int32_t n_topics) {
-  if (variant != WD_PREFIX || n_topics <= 0) return 0;
+  if (n_topics <= 0) return 0;
   size_t esz = dtype == WD_FLOAT64 ? 8 : 4;
+  // butterfly: the shared-vector search table (wd_sample_rows with ld = 0)
+  if (variant == WD_BUTTERFLY) return valid_lanes(lanes) ? shared_table_elems(lanes, n_topics) * esz : 0;
+  if (variant != WD_PREFIX) return 0;
   return (size_t)prefix_table_cols() * (size_t)n_topics * esz;
 }
 

@@ -11,6 +11,7 @@
 #include <utility>
 
 #include "wd_draw.cuh"
+#include "wd_shared.cuh"
 
 namespace wd {
 
@@ -151,12 +152,44 @@ int launch_bfly_w(int W, const DrawParams<T>& p, cudaStream_t st) {
   }
 }
 
+// one shared weight vector (ld = 0): table once, then one search per draw
+template <typename T, int W>
+int launch_shared_inst(const DrawParams<T>& p, void* ws, cudaStream_t st) {
+  T* tab = reinterpret_cast<T*>(ws);
+  shared_build_kernel<T, W><<<1, 256, 0, st>>>(p.phi, p.K, tab);
+  int64_t grid = (p.n_tokens + 255) / 256;
+  const int64_t cap = (int64_t)device_sm_count() * 8;
+  grid = grid > cap ? cap : grid;
+  shared_draw_kernel<T, W><<<(int)grid, 256, 0, st>>>(p, tab);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { set_last_cuda_error(e); return WD_ERR_CUDA; }
+  return WD_OK;
+}
+
+template <typename T>
+int launch_shared(int W, const DrawParams<T>& p, void* ws, cudaStream_t st) {
+  switch (W) {
+    case 2: return launch_shared_inst<T, 2>(p, ws, st);
+    case 4: return launch_shared_inst<T, 4>(p, ws, st);
+    case 8: return launch_shared_inst<T, 8>(p, ws, st);
+    case 16: return launch_shared_inst<T, 16>(p, ws, st);
+    case 32: return launch_shared_inst<T, 32>(p, ws, st);
+    case 64: return launch_shared_inst<T, 64>(p, ws, st);
+    default: return WD_ERR_UNSUPPORTED;
+  }
+}
+
 // Dispatch on (variant, W, VEC, MODE); explicit instantiations live in
 // wd_draw_f32.cu / wd_draw_f64.cu so the two element types compile in parallel.
 template <typename T>
 int launch_draw(int variant, int W, bool vec, int mode, const DrawParams<T>& p, void* ws,
                 size_t ws_bytes, cudaStream_t st) {
   if (variant == WD_BUTTERFLY) {
+    // shared vector with a table workspace: build once, search per draw
+    // (without one, every row runs the full per-row kernel: same results)
+    if (mode == MODE_ROWS && p.ld_phi == 0 && ws != nullptr &&
+        ws_bytes >= shared_table_elems(W, p.K) * sizeof(T))
+      return launch_shared<T>(W, p, ws, st);
     if (mode == MODE_LDA)
       return vec ? launch_bfly_w<T, true, MODE_LDA>(W, p, st) : launch_bfly_w<T, false, MODE_LDA>(W, p, st);
     return vec ? launch_bfly_w<T, true, MODE_ROWS>(W, p, st) : launch_bfly_w<T, false, MODE_ROWS>(W, p, st);

@@ -1,0 +1,77 @@
+"""Install the B200 path into a running `warpdraw` (the reference package).
+
+    import warpdraw
+    from paper_1505_03851_b200 import integrate
+    integrate.install()          # KERNELS / draw_z / SAMPLERS / gibbs path now run on the GPU
+
+After install():
+
+* warpdraw.kernels.KERNELS["basic" | "transposed" | "butterfly"] and
+  warpdraw.kernels.draw_z dispatch to the sm_100a kernels (same signatures,
+  exceptions and messages; kernels.py:542-555);
+* warpdraw.lda's own reference to draw_z is rebound, so gibbs_iterate /
+  run_gibbs (and `warpdraw lda --kernel ...`) draw on the GPU while keeping
+  the reference's numpy resample -- the results stay bit-identical;
+* warpdraw.bench.SAMPLERS["binary" | "alias" | "butterfly"] are the GPU
+  samplers (bench.py:150-154), bit-identical, and SAMPLERS["prefix"] (the
+  butterfly's u stream through a full prefix table) is added;
+* the reference's exception classes are the ones raised (AllZeroError,
+  StopOutOfRangeError are mapped).
+
+uninstall() restores the originals.
+"""
+
+from __future__ import annotations
+
+import importlib
+
+from . import kernels as _k
+from . import samplers as _s
+
+_saved: dict = {}
+
+
+def _wrap_errors(fn, ref_kernels, ref_sampling):
+    def call(*a, **kw):
+        try:
+            return fn(*a, **kw)
+        except _k.StopOutOfRangeError as exc:
+            raise ref_kernels.StopOutOfRangeError(str(exc)) from None
+        except _k.AllZeroError as exc:
+            raise ref_sampling.AllZeroError(str(exc)) from None
+
+    call.__name__ = getattr(fn, "__name__", "call")
+    call.__doc__ = fn.__doc__
+    return call
+
+
+def install(package: str = "warpdraw") -> None:
+    """Patch the imported reference package in place (idempotent)."""
+    if _saved:
+        return
+    ref_kernels = importlib.import_module(package + ".kernels")
+    ref_sampling = importlib.import_module(package + ".sampling")
+    ref_lda = importlib.import_module(package + ".lda")
+    ref_bench = importlib.import_module(package + ".bench")
+    _saved["kernels"] = (ref_kernels, dict(ref_kernels.KERNELS), ref_kernels.draw_z)
+    _saved["lda"] = (ref_lda, ref_lda.draw_z)
+    _saved["bench"] = (ref_bench, dict(ref_bench.SAMPLERS))
+    ref_kernels.KERNELS.update({name: _wrap_errors(fn, ref_kernels, ref_sampling) for name, fn in _k.KERNELS.items()})
+    gpu_draw_z = _wrap_errors(_k.draw_z, ref_kernels, ref_sampling)
+    ref_kernels.draw_z = gpu_draw_z
+    ref_lda.draw_z = gpu_draw_z
+    ref_bench.SAMPLERS.update(_s.SAMPLERS)
+
+
+def uninstall() -> None:
+    if not _saved:
+        return
+    ref_kernels, kernels, draw_z = _saved.pop("kernels")
+    ref_kernels.KERNELS.clear()
+    ref_kernels.KERNELS.update(kernels)
+    ref_kernels.draw_z = draw_z
+    ref_lda, lda_draw_z = _saved.pop("lda")
+    ref_lda.draw_z = lda_draw_z
+    ref_bench, samplers = _saved.pop("bench")
+    ref_bench.SAMPLERS.clear()
+    ref_bench.SAMPLERS.update(samplers)

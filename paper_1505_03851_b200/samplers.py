@@ -3,20 +3,27 @@ plus the batched independent-row API used by the K sweep (BASELINE configs[1]).
 
     sample_butterfly(weights, n, seed, lanes=8)   bench.py:129-147, on the GPU
     sample_prefix(weights, n, seed, lanes=8)      same u stream, prefix table
+    sample_binary(weights, n, seed)               bench.py:118-121, sequential xoshiro stream
+    sample_alias(weights, n, seed)                bench.py:123-126, exact Vose table
     sample_rows(weights[n, K], seed, ...)         one independent row per draw
 
 The u stream is units_for(derive_seed(seed, 6), draw_id) exactly as in
-bench.py:141-143; results are bit-identical to the reference.
+bench.py:141-143; results are bit-identical to the reference.  The binary
+and alias samplers consume ONE sequential xoshiro256** stream in the
+reference; on the device every thread jumps to its own stream position
+(wd_stream_draws), so they are bit-identical too.
 """
 
 from __future__ import annotations
+
+from fractions import Fraction
 
 import numpy as np
 
 from . import _lib
 from .kernels import StopOutOfRangeError, _workspace
 from .rng import derive_seed
-from .sampling import AllZeroError
+from .sampling import AllZeroError, EmptyWeightsError
 
 _VARIANTS = {"butterfly": _lib.WD_BUTTERFLY, "prefix": _lib.WD_PREFIX}
 
@@ -111,7 +118,93 @@ def sample_prefix(weights, n: int, seed: int, lanes: int = 8) -> np.ndarray:
     return _shared(weights, n, seed, lanes, "prefix")
 
 
+def _as_weights(weights) -> np.ndarray:
+    """sampling.py:27-33: non-empty 1-D float64, no negative entries."""
+    w = np.asarray(weights, dtype=np.float64)
+    if w.ndim != 1 or w.size == 0:
+        raise EmptyWeightsError("need a non-empty 1-D weight vector")
+    if np.any(w < 0):
+        raise ValueError("weights must be non-negative")
+    return w
+
+
+def alias_table(weights):
+    """Exact Vose alias table (sampling.py:101-131) as device-ready arrays.
+
+    Returns (thresh uint64[K], alias int32[K]) with thresh[k] =
+    ceil(F[k] * 2^53): for a 53-bit unit u = b * 2^-53 the reference's exact
+    test u < F[k] is b < thresh[k].  The worklists are stacks (pop from the
+    end) and a scaled weight of exactly 1 counts as large, so the pairing --
+    and hence every alias -- is the reference's.
+    """
+    w = _as_weights(weights)
+    exact = [Fraction(x) for x in w.tolist()]
+    total = sum(exact, Fraction(0))
+    if total <= 0:
+        raise AllZeroError("weights sum to zero")
+    K = len(exact)
+    scaled = [x * K / total for x in exact]
+    accept: list = [Fraction(1)] * K
+    alias = np.arange(K, dtype=np.int32)
+    small = [k for k, x in enumerate(scaled) if x < 1]
+    large = [k for k, x in enumerate(scaled) if x >= 1]
+    while small and large:
+        lo, hi = small.pop(), large.pop()
+        accept[lo], alias[lo] = scaled[lo], hi
+        scaled[hi] -= 1 - scaled[lo]
+        (small if scaled[hi] < 1 else large).append(hi)
+    # leftovers (either list) keep acceptance 1
+    thresh = np.array([-((-f.numerator << 53) // f.denominator) for f in accept], dtype=np.uint64)
+    return thresh, alias
+
+
+def _stream_draws(method, n, seed, table=None, thresh=None, alias=None, K=0):
+    import torch
+
+    _lib.require_cuda()
+    n = int(n)
+    if n < 0:
+        raise ValueError("n must be non-negative")
+    out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    L = _lib.load()
+    ws = torch.empty(int(L.wd_stream_workspace_bytes(n)), dtype=torch.uint8, device="cuda")
+    _lib.check(L.wd_stream_draws(method, _lib.ptr(table), _lib.ptr(thresh), _lib.ptr(alias), int(K),
+                                 int(seed) & ((1 << 64) - 1), n, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                 _lib.stream_handle()), "wd_stream_draws")
+    return out[:n].cpu().numpy().astype(np.int64)
+
+
+def sample_binary(weights, n: int, seed: int) -> np.ndarray:
+    """Prefix table + bisection, u from one xoshiro256** stream seeded
+    derive_seed(seed, 4) (bench.py:118-121, sampling.py:46-92)."""
+    import torch
+
+    w = _as_weights(weights)
+    if np.isnan(w).any() or not (w > 0).any():  # float64 running total not > 0
+        raise AllZeroError("weights sum to zero")
+    _lib.require_cuda()
+    wt = torch.from_numpy(np.ascontiguousarray(w)).cuda()
+    table = torch.empty_like(wt)
+    L = _lib.load()
+    _lib.check(L.wd_prefix_f64(wt.data_ptr(), wt.numel(), table.data_ptr(), _lib.stream_handle()), "wd_prefix_f64")
+    return _stream_draws(_lib.WD_STREAM_BINARY, n, derive_seed(int(seed), 4), table=table, K=w.size)
+
+
+def sample_alias(weights, n: int, seed: int) -> np.ndarray:
+    """Vose alias table, two units per draw from one xoshiro256** stream
+    seeded derive_seed(seed, 5) (bench.py:123-126, sampling.py:134-138)."""
+    import torch
+
+    thresh, alias = alias_table(weights)
+    _lib.require_cuda()
+    th = torch.from_numpy(thresh.view(np.int64)).cuda()
+    al = torch.from_numpy(alias).cuda()
+    return _stream_draws(_lib.WD_STREAM_ALIAS, n, derive_seed(int(seed), 5), thresh=th, alias=al, K=alias.size)
+
+
 SAMPLERS = {
+    "binary": sample_binary,
+    "alias": sample_alias,
     "butterfly": sample_butterfly,
     "prefix": sample_prefix,
 }

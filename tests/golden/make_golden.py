@@ -6,7 +6,7 @@ GPU box):
     python tests/golden/make_golden.py            # all fixtures
     python tests/golden/make_golden.py --skip-cfg1 # skip the ~4 min config-1 run
 
-Outputs (committed, small): tests/golden/{units,rows,lda,gibbs,cfg1}.npz.
+Outputs (committed, small): tests/golden/{units,rows,lda,gibbs,cfg1,stream}.npz.
 Each case records the exact reference call that produced it.  The oracle
 (oracle/wd_oracle.c) is pinned against these by tests/test_oracle.py; the
 CUDA product is checked against both by the -m gpu tests.
@@ -26,7 +26,8 @@ REF = os.environ.get("WARPDRAW_REF", "/root/reference/pkg/src")
 sys.path.insert(0, REF)
 
 from warpdraw import rng  # noqa: E402
-from warpdraw.bench import sample_butterfly  # noqa: E402
+from warpdraw.bench import sample_alias, sample_binary, sample_butterfly  # noqa: E402
+from warpdraw.sampling import build_alias_vose  # noqa: E402
 from warpdraw.kernels import (  # noqa: E402
     InjectedStops,
     SeededStops,
@@ -277,12 +278,43 @@ def gen_cfg1():
     print(f"cfg1 reference run_gibbs butterfly fp32 10 iters: {wall:.1f}s")
 
 
+def _stream_weights():
+    gen = np.random.default_rng(4242)
+    return {
+        "k19": gen.uniform(0.05, 1.0, size=19),
+        "k1": np.array([0.7]),
+        "uniform4": np.ones(4),  # every scaled weight exactly 1: all "large"
+        "ints": np.array([1.0, 2.0, 3.0, 2.0, 0.0, 8.0]),
+        "zeros": np.array([0.0, 0.0, 3.0, 0.0, 1e-300, 0.0, 5.0]),
+        "k200": gen.uniform(0.1, 1.0, size=200),
+        "k1000": gen.exponential(1.0, size=1000) ** 3,
+        "tiny": np.array([1e-310, 2e-310, 5e-324, 1e-310]),  # subnormal weights
+    }
+
+
+def gen_stream():
+    """SAMPLERS["binary"] / ["alias"] (bench.py:118-126): sequential
+    xoshiro256** draws; n covers many device threads' stream jumps."""
+    cases = {}
+    for i, (name, w) in enumerate(_stream_weights().items()):
+        n = 200_000 if name in ("k19", "k1000") else 5000
+        seed = 31 + 17 * i
+        cases[f"{name}/w"] = w
+        cases[f"{name}/seed"] = np.array(seed)
+        cases[f"{name}/binary"] = sample_binary(w, n, seed).astype(np.int16)
+        cases[f"{name}/alias"] = sample_alias(w, n, seed).astype(np.int16)
+        t = build_alias_vose(w)
+        cases[f"{name}/alias_A"] = np.asarray(t.A, dtype=np.int32)
+        cases[f"{name}/alias_T"] = np.array([-((-f.numerator << 53) // f.denominator) for f in t.F], dtype=np.uint64)
+    np.savez_compressed(os.path.join(OUT, "stream.npz"), **cases)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-cfg1", action="store_true")
     ap.add_argument("--only", default=None)
     args = ap.parse_args()
-    jobs = {"units": gen_units, "rows": gen_rows, "lda": gen_lda, "gibbs": gen_gibbs, "cfg1": gen_cfg1}
+    jobs = {"units": gen_units, "rows": gen_rows, "lda": gen_lda, "gibbs": gen_gibbs, "cfg1": gen_cfg1, "stream": gen_stream}
     for name, fn in jobs.items():
         if args.only and name != args.only:
             continue
