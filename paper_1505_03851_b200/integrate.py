@@ -16,7 +16,8 @@ After install():
   samplers (bench.py:150-154), bit-identical, and SAMPLERS["prefix"] (the
   butterfly's u stream through a full prefix table) is added;
 * the reference's exception classes are the ones raised (AllZeroError,
-  StopOutOfRangeError are mapped).
+  StopOutOfRangeError are mapped), and its SeededStops / InjectedStops
+  objects are recognised (in-kernel hash / u per token).
 
 uninstall() restores the originals.
 """
@@ -31,8 +32,21 @@ from . import samplers as _s
 _saved: dict = {}
 
 
+def _convert(x, ref_kernels):
+    """The reference's own stops providers map onto the device stop modes
+    (SeededStops -> in-kernel hash, InjectedStops -> u per token) instead of
+    the generic host-evaluated .units path; same values either way."""
+    if isinstance(x, ref_kernels.SeededStops):
+        return _k.SeededStops(x.seed)
+    if isinstance(x, ref_kernels.InjectedStops):
+        return _k.InjectedStops(x._units)
+    return x
+
+
 def _wrap_errors(fn, ref_kernels, ref_sampling):
     def call(*a, **kw):
+        a = tuple(_convert(x, ref_kernels) for x in a)
+        kw = {k: _convert(v, ref_kernels) for k, v in kw.items()}
         try:
             return fn(*a, **kw)
         except _k.StopOutOfRangeError as exc:

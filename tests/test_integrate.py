@@ -47,3 +47,15 @@ def test_install_patches_and_restores(warpdraw):
     assert warpdraw.kernels.draw_z is orig_draw
     assert warpdraw.kernels.KERNELS == orig_kernels
     assert "prefix" not in warpdraw.bench.SAMPLERS
+
+
+def test_reference_stops_objects_are_recognised(warpdraw):
+    from paper_1505_03851_b200 import integrate, kernels
+
+    s = integrate._convert(warpdraw.kernels.SeededStops(5), warpdraw.kernels)
+    assert isinstance(s, kernels.SeededStops) and s.seed == 5
+    inj = warpdraw.kernels.InjectedStops([[0.25, 0.5], [], [0.75]])
+    j = integrate._convert(inj, warpdraw.kernels)
+    assert isinstance(j, kernels.InjectedStops)
+    assert [list(u) for u in j._units] == [[0.25, 0.5], [], [0.75]]
+    assert integrate._convert(3, warpdraw.kernels) == 3
