@@ -42,7 +42,8 @@ enum { MODE_LDA = 0, MODE_ROWS = 1 };
 #define WD_LDA_MIN_BLOCKS 6
 #endif
 #ifndef WD_LDA_MIN_BLOCKS_COARSE  // K > 32 * W: the group recompute needs more registers
-#define WD_LDA_MIN_BLOCKS_COARSE 4
+                                   // (measured at K = 4096: 4 -> 463 ms, 5 -> 415, 6 -> 468 per cfg5 draw)
+#define WD_LDA_MIN_BLOCKS_COARSE 5
 #endif
 
 template <typename T> struct DrawParams {
@@ -494,7 +495,14 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
                (size_t)wib * RingDepth<PIPE>::NS * RingStage<W>::BYTES;
   const int s = lane % L;
   const int rg = lane / L;
-  const int own = s * R + rg;  // chunk row this lane ends up owning
+  // Chunk row of the lane's kk-th load.  LDA: each lane group rg loads L
+  // CONSECUTIVE rows (a warp instruction still reads R full row segments),
+  // so a lane's rows span few documents and their theta segments are shared
+  // (per-lane ND = 2 below); rows: interleaved.  The transpose-reduce leaves
+  // lane (s, rg) with the total of its kk = s row.
+  constexpr bool CONTIG = MODE == MODE_LDA;
+  auto row_of = [&](int kk) { return CONTIG ? rg * L + kk : kk * R + rg; };
+  const int own = row_of(s);  // chunk row this lane ends up owning
   const int64_t n = p.n_tokens;
   const int64_t n_chunks = (n + 31) >> 5;
   const int64_t wpb = blockDim.x >> 5;
@@ -518,7 +526,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
     bool rvalid[L];
 #pragma unroll
     for (int kk = 0; kk < L; ++kk) {
-      const int k = kk * R + rg;
+      const int k = row_of(kk);
       rvalid[kk] = tok0 + k < n;
       if (MODE == MODE_LDA) {
         // invalid rows read word 0 / doc 0 (valid memory); their sums are discarded
@@ -551,7 +559,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
 #pragma unroll
       for (int kk = 0; kk < L; ++kk) {
         if (s * E < rem) {
-          const int k = kk * R + rg;
+          const int k = row_of(kk);
 #pragma unroll
           for (int c = 0; c < (int)(E * sizeof(T) / 16); ++c)
             cp_async16(RT + k * TS + s * E + c * (16 / sizeof(T)), prow.ptr(kk, -rem + c * (16 / (int)sizeof(T))));
@@ -567,7 +575,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
 #pragma unroll
         for (int kk = h; kk < h + HB; ++kk) {
           if (s * E < rem) {
-            const int k = kk * R + rg;
+            const int k = row_of(kk);
             const bool full = s * E + E <= rem;  // else: partial segment, scalar loads
             Seg<T, E, VEC> x;
             if (full) x.load(prow.ptr(kk, -rem)); else load_first(x.v, prow.ptr(kk, -rem), rem - s * E);
@@ -591,9 +599,12 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
       for (int t = 0; t < rem; ++t) prem = add_rn(prem, RT[own * TS + t]);  // sequential
       acc = prem;
     }
-    // theta rows the chunk needs: one document (ND=1), two (ND=2: the rows of
-    // the second one are flagged in dsel), or more (ND=0: per-row loads).
-    // Chunks are CSR-ordered, so their documents are nondecreasing.
+    // theta rows: one document for the whole chunk (ND = 1), else ND = 2
+    // with the first and last document of the LANE's rows (its L rows are
+    // consecutive; each lane loads its own pair of theta segments, a warp
+    // instruction still covering R row segments), the rows of the second
+    // flagged in dsel; ND = 0 (per-row theta loads) only when some lane's
+    // rows touch three documents.
     int nd = 1;
     uint32_t dsel = 0;
     RowSet<T, LT> trow_nd = trow;
@@ -601,15 +612,23 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
       const int32_t d0 = __shfl_sync(FULL, my_doc, 0);
       const int32_t d1 = __reduce_max_sync(FULL, my_valid ? my_doc : d0);
       if (d1 != d0) {
-        nd = __all_sync(FULL, !my_valid || my_doc == d0 || my_doc == d1) ? 2 : 0;
-        if (nd == 2) {
+        const uint32_t da = trow.idx[0];
+        uint32_t db = da;
 #pragma unroll
-          for (int kk = 0; kk < L; ++kk) {
-            const int32_t dk = __shfl_sync(FULL, my_doc, kk * R + rg);
-            if (dk == d1 && rvalid[kk]) dsel |= 1u << kk;
-          }
-          trow_nd.idx[0] = (uint32_t)d0;
-          trow_nd.idx[1] = (uint32_t)d1;
+        for (int kk = 0; kk < L; ++kk)
+          if (rvalid[kk]) db = trow.idx[kk];
+        bool ok = true;
+#pragma unroll
+        for (int kk = 0; kk < L; ++kk) {
+          ok = ok && (!rvalid[kk] || trow.idx[kk] == da || trow.idx[kk] == db);
+          if (rvalid[kk] && trow.idx[kk] != da) dsel |= 1u << kk;
+        }
+        nd = __all_sync(FULL, ok) ? 2 : 0;
+        if (nd == 2) {
+          trow_nd.idx[0] = da;
+          trow_nd.idx[1] = db;
+        } else {
+          dsel = 0;
         }
       } else {
         trow_nd.idx[0] = (uint32_t)d0;
@@ -679,7 +698,6 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
       // running sum exceeds stop (S is nondecreasing, so any search that finds
       // that block is the reference's bisection)
       T cur[W];
-      bool have_cur = false;
       int j;
       T prev, high;
       auto load_block = [&](int64_t base) {  // own row's products of one block
@@ -731,7 +749,6 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
             }
             run = sb;
           }
-          have_cur = true;
         }
       }
       const int64_t bb = (int64_t)rem + (int64_t)j * W;
@@ -740,7 +757,8 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
       int result = 0;
       if (nb > 0 && !fallback) {
         // rebuild the selected block's products (own row) and walk it
-        if (!COARSE || !have_cur) load_block(bb);
+        load_block(bb);  // coarse: reloaded (L1 hit) rather than kept live, which
+                         // lets the coarse kernel fit 5 CTAs per SM
         T low = prev;
         int lo = 0;
         Walk<T, W / 2>::run(cur, low, high, stop, r, lo);

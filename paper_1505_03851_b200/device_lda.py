@@ -5,9 +5,11 @@ One Gibbs iteration (lda.py:211-242 semantics, uncollapsed):
     word_topic = 0
     z ~ draw (butterfly kernel, SeededStops(derive_seed(seed, 1, t)))
         with word_topic += 1 fused into the draw epilogue
-    all_reduce(word_topic, SUM)                      # NCCL, only if sharded
-    phi[:, k]  ~ Dir(beta + word_topic[:, k])        # wd_resample_phi
+    all_reduce(word_topic, SUM)                      # NCCL, only if sharded:
+        per vocabulary tile, enqueued behind that tile's draw launch, so it
+        overlaps the next tile's draw
     theta[m]   ~ Dir(alpha + hist(z of doc m))       # wd_resample_theta
+    phi[:, k]  ~ Dir(beta + word_topic[:, k])        # wd_resample_phi
 
 Documents are sharded across ranks in 32-aligned contiguous ranges; the
 global doc id drives both the u hash and the theta Gamma stream, and phi is
@@ -22,6 +24,7 @@ import numpy as np
 from . import _lib
 from .kernels import DeviceCorpus, SeededStops, combine_err, draw_z_device, raise_for_err
 from .rng import derive_seed
+from .sharding import TileAllReduce, count_chunks
 
 # phi slice kept L2-resident per draw pass (126 MB L2; measured: 41 MB slices
 # run at the L2-resident rate, 82 MB ones do not -- profiles/)
@@ -60,6 +63,7 @@ class DeviceLDA:
         if vocab_tile_bytes and self.V * self.K * esz > vocab_tile_bytes:
             rows = max(1, int(vocab_tile_bytes // (self.K * esz)))
             self.tiles = corpus.vocab_tiles(rows)
+        self._reducer = None  # in-flight per-tile count all-reduces (draw -> resample)
         n_err = self.tiles.n_tiles if self.tiles is not None else 1
         self.err = torch.empty((n_err, 2), dtype=torch.int64, device=dev)
 
@@ -95,29 +99,48 @@ class DeviceLDA:
         self.resample(t)
 
     # ------------------------------------------------------- one sweep
-    def draw(self, t: int, fused_counts: bool = True):
+    def draw(self, t: int, fused_counts: bool = True, overlap_allreduce: bool = False):
+        """z draw with the word_topic counts fused.  overlap_allreduce (sharded
+        runs): tile t's count rows are final as soon as its launch retires, so
+        their all-reduce is enqueued right behind it and runs on the NCCL
+        stream while the next tile draws; the works are kept for resample()."""
         self.word_topic.zero_()
+        self._reducer = None
+        after = None
+        if overlap_allreduce and self.pg is not None and fused_counts:
+            dist = self.torch.distributed
+            self._reducer = TileAllReduce(
+                self.word_topic, count_chunks(self.V, self.tiles.rows_per_tile if self.tiles is not None else None),
+                lambda v: dist.all_reduce(v, group=self.pg, async_op=True))
+            after = self._reducer.after_tile
         draw_z_device(self.kernel, self.corpus, self.theta, self.phi, SeededStops(derive_seed(self.seed, 1, t)),
                       self.lanes, z=self.z, word_topic=self.word_topic if fused_counts else None, err=self.err,
-                      check=False, tiles=self.tiles)
+                      check=False, tiles=self.tiles, after_tile=after)
+        if self._reducer is not None:
+            self._reducer.finish()
 
     def allreduce_counts(self):
-        if self.pg is not None:
+        if self.pg is not None and getattr(self, "_reducer", None) is None:
             self.torch.distributed.all_reduce(self.word_topic, group=self.pg)
 
     def resample(self, t: int):
         L = _lib.load()
         st = _lib.stream_handle()
-        _lib.check(L.wd_resample_phi(self._dt, self.word_topic.data_ptr(), self.V, self.K, self.beta,
-                                     derive_seed(self.seed, 2, t, 1), self.phi.data_ptr(), self.phi.stride(0),
-                                     self._phi_ws.data_ptr(), self._phi_ws.numel(), st), "wd_resample_phi")
+        # theta needs only the local z: it runs while in-flight count
+        # all-reduces finish; phi waits for them
         _lib.check(L.wd_resample_theta(self._dt, self.z.data_ptr(), self.corpus.offsets.data_ptr(),
                                        self.corpus.n_docs, self.K, self.alpha, derive_seed(self.seed, 2, t, 0),
                                        self.corpus.doc_base, self.theta.data_ptr(), self.theta.stride(0), st),
                    "wd_resample_theta")
+        if getattr(self, "_reducer", None) is not None:
+            self._reducer.wait()
+            self._reducer = None
+        _lib.check(L.wd_resample_phi(self._dt, self.word_topic.data_ptr(), self.V, self.K, self.beta,
+                                     derive_seed(self.seed, 2, t, 1), self.phi.data_ptr(), self.phi.stride(0),
+                                     self._phi_ws.data_ptr(), self._phi_ws.numel(), st), "wd_resample_phi")
 
-    def iterate(self, t: int):
-        self.draw(t)
+    def iterate(self, t: int, overlap_allreduce: bool = True):
+        self.draw(t, overlap_allreduce=overlap_allreduce)
         self.allreduce_counts()
         self.resample(t)
 

@@ -325,7 +325,7 @@ def raise_for_err(err_host, key_rule: int, lanes: int):
 
 def draw_z_device(kernel: str, corpus: DeviceCorpus, theta, phi, stops, lanes: int = 32, *, z=None,
                   word_topic=None, doc_topic=None, err=None, check: bool = True, stream=None,
-                  tiles: VocabTiles | None = None):
+                  tiles: VocabTiles | None = None, after_tile=None):
     """Device-resident draw.  theta [n_docs, K], phi [V, K] CUDA tensors
     (float32 or float64, same dtype, row stride = leading dim).  Returns z
     (int32 CUDA tensor, CSR token order).  word_topic / doc_topic (int32) are
@@ -333,7 +333,11 @@ def draw_z_device(kernel: str, corpus: DeviceCorpus, theta, phi, stops, lanes: i
     draws tile by tile so each phi slice stays L2-resident; z is identical.
     check=False skips the host synchronisation on the error word (err, shape
     [n_launches, 2], must then be supplied and inspected by the caller with
-    raise_for_err(combine_err(err)))."""
+    raise_for_err(combine_err(err))).  after_tile(t, word_lo, word_hi) is
+    called right after tile t's launch is enqueued: the word_topic rows
+    [word_lo, word_hi) are final on the stream from that point (a tile's
+    tokens are exactly the words of its range), which lets a caller start
+    their all-reduce while the next tile draws."""
     torch = _torch()
     if kernel not in _KERNEL_SPEC:
         raise ValueError(f"unknown kernel {kernel!r}; pick one of {sorted(_KERNEL_SPEC)}")
@@ -358,10 +362,10 @@ def draw_z_device(kernel: str, corpus: DeviceCorpus, theta, phi, stops, lanes: i
     if z is None:
         z = torch.empty(corpus.n_tokens, dtype=torch.int32, device=dev)
     if tiles is None:
-        launches = [(corpus.words, corpus.token_doc, None, 0, corpus.n_tokens)]
+        launches = [(corpus.words, corpus.token_doc, None, 0, corpus.n_tokens, 0)]
     else:
-        launches = [(tiles.words, tiles.token_doc, tiles.token_pos, a, b - a)
-                    for a, b in zip(tiles.bounds[:-1], tiles.bounds[1:]) if b > a]
+        launches = [(tiles.words, tiles.token_doc, tiles.token_pos, a, b - a, t)
+                    for t, (a, b) in enumerate(zip(tiles.bounds[:-1], tiles.bounds[1:])) if b > a]
     if err is None or err.numel() < 2 * max(1, len(launches)):
         err = torch.empty((max(1, len(launches)), 2), dtype=torch.int64, device=dev)
     err2 = err.view(-1, 2)
@@ -369,7 +373,7 @@ def draw_z_device(kernel: str, corpus: DeviceCorpus, theta, phi, stops, lanes: i
     ws, ws_bytes = _workspace(variant, dt, lanes, K, dev)
     L = _lib.load()
     st = _lib.stream_handle(stream)
-    for li, (wds, tdoc, tpos, a, n) in enumerate(launches):
+    for li, (wds, tdoc, tpos, a, n, t) in enumerate(launches):
         _lib.check(
             L.wd_draw_z(variant, dt, int(lanes), theta.data_ptr(), theta.stride(0), phi.data_ptr(), phi.stride(0), K,
                         corpus.offsets.data_ptr(), wds.data_ptr() + 4 * a, tdoc.data_ptr() + 4 * a,
@@ -378,6 +382,10 @@ def draw_z_device(kernel: str, corpus: DeviceCorpus, theta, phi, stops, lanes: i
                         z.data_ptr(), _lib.ptr(word_topic), _lib.ptr(doc_topic), err2[li].data_ptr(), _lib.ptr(ws),
                         ws_bytes, st),
             "wd_draw_z")
+        if after_tile is not None:
+            V = int(phi.shape[0])
+            lo, hi = (0, V) if tiles is None else (t * tiles.rows_per_tile, min(V, (t + 1) * tiles.rows_per_tile))
+            after_tile(t, lo, hi)
     if not launches:
         err2.zero_()
         err2[:, 0] = -1

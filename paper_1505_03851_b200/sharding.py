@@ -43,3 +43,50 @@ def shard_csr(offsets, words, lo: int, hi: int):
     offsets = np.asarray(offsets, dtype=np.int64)
     a, b = int(offsets[lo]), int(offsets[hi])
     return offsets[lo : hi + 1] - a, np.asarray(words)[a:b]
+
+
+def count_chunks(vocab_size: int, rows_per_tile: int | None):
+    """word_topic row ranges reduced one by one: the vocabulary tiles, derived
+    from V and the tile height only, so every rank has the same list."""
+    if not rows_per_tile:
+        return [(0, int(vocab_size))]
+    return [(lo, min(int(vocab_size), lo + int(rows_per_tile))) for lo in range(0, int(vocab_size), int(rows_per_tile))]
+
+
+class TileAllReduce:
+    """Issues the word-topic count all-reduce tile by tile behind the draw.
+
+    A vocabulary tile's draw touches only the count rows of its own words,
+    so once its launch is enqueued those rows are final on the stream and
+    their all-reduce can run (NCCL stream) while the next tile draws.  Ranks
+    skip launches for tiles their shard has no tokens in, so issuing is
+    driven by the row range reached, not by launch count: every rank issues
+    the same chunk sequence in the same order (a collective requirement).
+
+    all_reduce(view) -> work (with .wait()) is the collective, e.g.
+    lambda v: dist.all_reduce(v, group=pg, async_op=True).
+    """
+
+    def __init__(self, counts, chunks, all_reduce):
+        self.counts = counts
+        self.chunks = list(chunks)
+        self.all_reduce = all_reduce
+        self.next = 0
+        self.works = []
+
+    def after_tile(self, t, lo, hi):
+        while self.next < len(self.chunks) and self.chunks[self.next][1] <= hi:
+            a, b = self.chunks[self.next]
+            self.works.append(self.all_reduce(self.counts[a:b]))
+            self.next += 1
+
+    def finish(self):
+        """Issue the chunks no launch reached (tiles empty on this rank)."""
+        if self.chunks:
+            self.after_tile(-1, self.chunks[-1][1], self.chunks[-1][1])
+        return self.works
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+        self.works = []

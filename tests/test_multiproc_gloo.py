@@ -80,3 +80,55 @@ def test_two_rank_gloo_matches_single_process(tmp_path):
     np.testing.assert_array_equal(z_parts, z_full)
     for r in range(world):
         np.testing.assert_array_equal(np.load(tmp_path / f"wt{r}.npy"), wt_full)
+
+
+def _tile_worker(rank, world, port, out_dir):
+    """Per-tile overlapped all-reduce (sharding.TileAllReduce as DeviceLDA
+    drives it): counts are produced tile by tile, each rank skips the tiles
+    its shard has no tokens in, and the collective sequence must still line
+    up across ranks and give the full counts."""
+    from oracle import oracle as O
+    from paper_1505_03851_b200.sharding import TileAllReduce, count_chunks
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    M, V, K, N, off, words, theta, phi = _problem()
+    # rank 1 has no tokens in words [40, 80): drop them from its shard
+    lo, hi = shard_ranges(N, world)[rank]
+    soff, swords = shard_csr(off, words, lo, hi)
+    z, err = O.draw_z_csr(theta[lo:hi], phi, soff, swords, W=32, seed=O.derive_seed(7, 1, 0), doc_base=lo)
+    keep = np.ones(swords.size, bool) if rank == 0 else ~((swords >= 40) & (swords < 80))
+    rows = 20
+    wt = torch.zeros((V, K), dtype=torch.int32)
+    red = TileAllReduce(wt, count_chunks(V, rows), lambda v: dist.all_reduce(v, async_op=True))
+    tile = swords // rows
+    for t in range(int(tile.max()) + 1):
+        sel = keep & (tile == t)
+        if not sel.any():
+            continue  # no launch for an empty tile
+        np.add.at(wt.numpy(), (swords[sel], z[sel]), 1)
+        red.after_tile(t, t * rows, min(V, (t + 1) * rows))
+    red.finish()
+    red.wait()
+    local = np.zeros((V, K), np.int64)
+    np.add.at(local, (swords[keep], z[keep]), 1)
+    np.save(os.path.join(out_dir, f"tiles_wt{rank}.npy"), wt.numpy())
+    np.save(os.path.join(out_dir, f"tiles_local{rank}.npy"), local)
+    dist.destroy_process_group()
+
+
+def test_count_chunks_cover_vocab():
+    from paper_1505_03851_b200.sharding import count_chunks
+
+    assert count_chunks(100, None) == [(0, 100)]
+    c = count_chunks(101, 20)
+    assert c[0] == (0, 20) and c[-1] == (100, 101) and all(c[i][1] == c[i + 1][0] for i in range(len(c) - 1))
+
+
+def test_two_rank_gloo_tile_allreduce(tmp_path):
+    world = 2
+    mp.start_processes(_tile_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    total = sum(np.load(tmp_path / f"tiles_local{r}.npy") for r in range(world))
+    for r in range(world):
+        np.testing.assert_array_equal(np.load(tmp_path / f"tiles_wt{r}.npy"), total)
