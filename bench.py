@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sampler", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="create the NCCL process group even at world size 1 (exercises the N>1 code path)")
     return ap.parse_args()
 
 
@@ -249,8 +251,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if world > 1 or args.force_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
         pg = dist.group.WORLD
     K, V = args.topics, args.vocab
     peak, peak_src = load_peaks()
@@ -267,7 +271,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def barrier():
-        if world > 1:
+        if pg is not None:
             dist.barrier()
 
     for t in range(args.warmup):
@@ -300,7 +304,7 @@ def main():
     draw_avg = sum(a.elapsed_time(b) for a, b in d_ev) / len(d_ev) / 1e3
     red = torch.tensor([elapsed, draw_avg], dtype=torch.float64, device=dev)
     tot = torch.tensor([float(n_tok)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if pg is not None:
         dist.all_reduce(red, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
     elapsed, draw_avg = float(red[0]), float(red[1])
@@ -329,8 +333,10 @@ def main():
         h_z = torch.empty(n_tok, dtype=torch.int32).pin_memory()
         h2d = h_theta.numel() * h_theta.element_size() + h_phi.numel() * h_phi.element_size()
         d2h = n_tok * 4
-        th_buf = [lda.theta, torch.empty_like(lda.theta)]
-        ph_buf = [lda.phi, torch.empty_like(lda.phi)]
+        from paper_1505_03851_b200.kernels import block_aligned_rows
+
+        th_buf = [lda.theta, block_aligned_rows(*lda.theta.shape, lda.theta.dtype, dev)]
+        ph_buf = [lda.phi, block_aligned_rows(*lda.phi.shape, lda.phi.dtype, dev)]
         z_buf = [lda.z, torch.empty_like(lda.z)]
         up, down = torch.cuda.Stream(), torch.cuda.Stream()
         ready = [torch.cuda.Event() for _ in range(2)]
@@ -371,7 +377,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         et = torch.tensor([a.elapsed_time(b) / 1e3 / n_e2e], dtype=torch.float64, device=dev)
-        if world > 1:
+        if pg is not None:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         lda.check_errors()
         e2e = {"value": total_tokens / float(et[0]), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
@@ -487,7 +493,7 @@ def main():
             "sampler": sampler,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if pg is not None:
         dist.destroy_process_group()
 
 

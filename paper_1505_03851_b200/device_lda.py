@@ -22,7 +22,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from .kernels import DeviceCorpus, SeededStops, combine_err, draw_z_device, raise_for_err
+from .kernels import DeviceCorpus, SeededStops, block_aligned_rows, combine_err, draw_z_device, raise_for_err
 from .rng import derive_seed
 from .sharding import TileAllReduce, count_chunks
 
@@ -49,8 +49,9 @@ class DeviceLDA:
         self.pg = process_group
         dev = corpus.offsets.device
         self.device = dev
-        self.theta = theta if theta is not None else torch.empty((corpus.n_docs, self.K), dtype=self.dtype, device=dev)
-        self.phi = phi if phi is not None else torch.empty((self.V, self.K), dtype=self.dtype, device=dev)
+        # line-aligned W-topic blocks (kernels.block_aligned_rows)
+        self.theta = theta if theta is not None else block_aligned_rows(corpus.n_docs, self.K, self.dtype, dev, lanes)
+        self.phi = phi if phi is not None else block_aligned_rows(self.V, self.K, self.dtype, dev, lanes)
         self.z = torch.zeros(corpus.n_tokens, dtype=torch.int32, device=dev)
         self.word_topic = torch.zeros((self.V, self.K), dtype=torch.int32, device=dev)
         L = _lib.load()

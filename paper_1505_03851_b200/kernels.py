@@ -29,6 +29,7 @@ from .warp import Trace, WarpConfig
 
 __all__ = [
     "VocabTiles",
+    "block_aligned_rows",
     "combine_err",
     "StopOutOfRangeError",
     "SeededStops",
@@ -237,6 +238,32 @@ def _build_vocab_tiles(corpus: "DeviceCorpus", rows_per_tile: int) -> VocabTiles
     return VocabTiles(words, doc, pos, [int(b) for b in bounds], int(rows_per_tile))
 
 
+def block_aligned_rows(n_rows: int, K: int, dtype=None, device=None, lanes: int = 32):
+    """An [n_rows, K] theta/phi buffer whose W-topic blocks start on 128-byte
+    lines: a view into a row-padded allocation, offset so that column
+    K mod W (the first block; the remnant comes first, kernels.py:199-205)
+    is line-aligned, with a leading dimension of whole lines.  With K = 200 a
+    dense row is 800 B and every 128-byte block segment straddles two L1/L2
+    lines (two wavefronts per row per load); aligned, it touches one.  Same
+    values, same results, ~12% more memory at K = 200, none when K % 32 == 0."""
+    torch = _torch()
+    dtype = dtype or torch.float32
+    esz = torch.empty(0, dtype=dtype).element_size()
+    line = 128 // esz
+    lead = (-(K % lanes)) % line
+    ld = -(-(lead + K) // line) * line
+    if lead == 0 and ld == K:
+        return torch.empty((n_rows, K), dtype=dtype, device=device)
+    return torch.empty((n_rows, ld), dtype=dtype, device=device)[:, lead : lead + K]
+
+
+def to_block_aligned(t, lanes: int = 32):
+    """Copy of a 2-D CUDA tensor in the block_aligned_rows layout."""
+    out = block_aligned_rows(t.shape[0], t.shape[1], t.dtype, t.device, lanes)
+    out.copy_(t)
+    return out
+
+
 _DTYPES = {"float32": _lib.WD_FLOAT32, "float64": _lib.WD_FLOAT64}
 
 
@@ -425,8 +452,8 @@ def _host_call(kernel, N, theta, phi, w, lanes, stops, trace, threads, step_hook
     _lib.require_cuda()
     corpus = DeviceCorpus.from_ragged(N, w)
     dev = torch.device("cuda")
-    th = torch.from_numpy(np.ascontiguousarray(theta)).to(dev)
-    ph = torch.from_numpy(np.ascontiguousarray(phi.astype(theta.dtype, copy=False))).to(dev)
+    th = to_block_aligned(torch.from_numpy(np.ascontiguousarray(theta)).to(dev), lanes)
+    ph = to_block_aligned(torch.from_numpy(np.ascontiguousarray(phi.astype(theta.dtype, copy=False))).to(dev), lanes)
     z = draw_z_device(kernel, corpus, th, ph, stops, lanes)
     return _to_host_ragged(z, N)
 
