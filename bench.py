@@ -225,7 +225,11 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"lda_k{K}_draw_cpu", "topics": K, "vocab": V, "lanes": 32},
+        # the same workload as the GPU arm; each step is a bounded document
+        # sample of it (cpu_baseline.sample), draw only (no resample)
+        "config": {"workload": f"lda_cfg4_k{K}", "docs_per_gpu": args.docs_per_gpu, "vocab": V, "topics": K,
+                   "mean_doc_len": args.mean_len, "kernel": "butterfly", "lanes": 32,
+                   "parallelism": "host cores (rank 0 only)", "sample_docs_per_step": S},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
