@@ -510,12 +510,17 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
   const uint64_t pol_t = make_l2_policy(p.l2_policy_t);
   for (int64_t c = (int64_t)blockIdx.x * wpb + wib; c < n_chunks; c += (int64_t)gridDim.x * wpb) {
     const int64_t tok0 = c << 5;
-    const bool my_valid = tok0 + lane < n;
+    bool my_valid = tok0 + lane < n;
     int32_t my_doc = 0, my_word = 0;
     if (MODE == MODE_LDA && my_valid) {
       my_doc = p.token_doc[tok0 + lane];
       my_word = p.words[tok0 + lane];
+      // padding slot of a run-padded vocabulary tile (token_pos < 0): it
+      // carries its run's document and a word of it (valid loads, so the
+      // lane group stays single-document) but draws nothing
+      if (p.token_pos != nullptr) my_valid = p.token_pos[tok0 + lane] >= 0;
     }
+    const uint32_t vmask = __ballot_sync(FULL, my_valid);
     constexpr int LT = L < 2 ? 2 : L;
     RowSet<T, L> prow;  // the L rows this lane loads (phi / weights)
     RowSet<T, LT> trow;  // their theta rows (LDA)
@@ -527,10 +532,19 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
 #pragma unroll
     for (int kk = 0; kk < L; ++kk) {
       const int k = row_of(kk);
-      rvalid[kk] = tok0 + k < n;
+      rvalid[kk] = (vmask >> k) & 1u;
       if (MODE == MODE_LDA) {
-        // invalid rows read word 0 / doc 0 (valid memory); their sums are discarded
-        prow.idx[kk] = (uint32_t)__shfl_sync(FULL, my_word, k);
+        // an invalid row (run padding, chunk tail) reads the phi row of a
+        // valid row of the SAME load instruction (rows k ^ j*L), so the
+        // coalescer merges it and it costs no extra L1/L2 traffic; its theta
+        // stays its own run's document (the lane group's); sums discarded
+        int src = k;
+        if (!COARSE && !rvalid[kk]) {
+#pragma unroll
+          for (int j = R - 1; j >= 1; --j)
+            if ((vmask >> (k ^ (j * L))) & 1u) src = k ^ (j * L);
+        }
+        prow.idx[kk] = (uint32_t)__shfl_sync(FULL, my_word, src);
         trow.idx[kk] = (uint32_t)__shfl_sync(FULL, my_doc, k);
       } else {
         prow.idx[kk] = (uint32_t)(rvalid[kk] ? tok0 + k : tok0);
@@ -539,7 +553,7 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
     }
     if (L < 2) trow.idx[LT - 1] = trow.idx[0];
     const int64_t own_tok = tok0 + own;
-    const bool own_valid = own_tok < n;
+    const bool own_valid = (vmask >> own) & 1u;
     const int32_t own_doc = __shfl_sync(FULL, my_doc, own);
     const int32_t own_word = __shfl_sync(FULL, my_word, own);
     const T* pown = p.phi + (MODE == MODE_LDA ? (int64_t)own_word : own_tok) * p.ld_phi;
@@ -624,7 +638,15 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
           if (rvalid[kk] && trow.idx[kk] != da) dsel |= 1u << kk;
         }
         nd = __all_sync(FULL, ok) ? 2 : 0;
-        if (nd == 2) {
+        if (!COARSE && nd == 2 && __all_sync(FULL, dsel == 0u)) {
+          // every lane's rows are one document (per lane group; always so
+          // on run-padded tiles): one theta segment per lane, no per-row
+          // selection.  Fine instantiation only: in the coarse one the extra
+          // path costs more (register allocation) than it saves unpadded
+          // (measured at K = 4096: 420 vs 443 ms)
+          nd = 1;
+          trow_nd.idx[0] = da;
+        } else if (nd == 2) {
           trow_nd.idx[0] = da;
           trow_nd.idx[1] = db;
         } else {
@@ -815,11 +837,12 @@ __global__ void __launch_bounds__(128) prefix_kernel(DrawParams<T> p, T* __restr
   const int WR = p.lanes;
   for (int64_t c = (int64_t)blockIdx.x * wpb + wib; c < n_chunks; c += (int64_t)gridDim.x * wpb) {
     const int64_t tok0 = c << 5;
-    const bool my_valid = tok0 + lane < n;
+    bool my_valid = tok0 + lane < n;
     int32_t my_doc = 0, my_word = 0;
     if (MODE == MODE_LDA && my_valid) {
       my_doc = p.token_doc[tok0 + lane];
       my_word = p.words[tok0 + lane];
+      if (p.token_pos != nullptr) my_valid = p.token_pos[tok0 + lane] >= 0;  // padding slot
     }
     const T* pown = p.phi + (MODE == MODE_LDA ? (int64_t)my_word : tok0 + lane) * p.ld_phi;
     const T* town = MODE == MODE_LDA ? p.theta + (int64_t)my_doc * p.ld_theta : nullptr;

@@ -29,12 +29,16 @@ from .sharding import TileAllReduce, count_chunks
 # phi slice kept L2-resident per draw pass (126 MB L2; measured: 41 MB slices
 # run at the L2-resident rate, 82 MB ones do not -- profiles/)
 DEFAULT_VOCAB_TILE_BYTES = 40 << 20
+# mean tokens per (document, tile) run from which runs are padded to the
+# butterfly kernel's lane-group height (VocabTiles.run_pad)
+RUN_PAD_MIN_MEAN_RUN = 20  # measured at K=1024 (runs ~50 tokens): draw -10%
 
 
 class DeviceLDA:
     def __init__(self, corpus: DeviceCorpus, n_topics: int, vocab_size: int, *, lanes: int = 32, dtype=None,
                  alpha: float = 0.1, beta: float = 0.01, seed: int = 0, kernel: str = "butterfly",
-                 process_group=None, theta=None, phi=None, vocab_tile_bytes: int | None = DEFAULT_VOCAB_TILE_BYTES):
+                 process_group=None, theta=None, phi=None, vocab_tile_bytes: int | None = DEFAULT_VOCAB_TILE_BYTES,
+                 run_pad: int | None = None):
         import torch
 
         _lib.require_cuda()
@@ -63,7 +67,16 @@ class DeviceLDA:
         self.tiles = None
         if vocab_tile_bytes and self.V * self.K * esz > vocab_tile_bytes:
             rows = max(1, int(vocab_tile_bytes // (self.K * esz)))
-            self.tiles = corpus.vocab_tiles(rows)
+            if run_pad is None:
+                # pad (tile, document) runs to the lane-group height when runs
+                # are long enough that the padding (~L/2 slots per run) costs
+                # less than the two-document theta selection it removes
+                n_tiles = -(-self.V // rows)
+                mean_run = corpus.n_tokens / max(1, corpus.n_docs) / n_tiles
+                # (fine instantiation only: at most 32 blocks per row)
+                fine = self.K // self.lanes <= 32
+                run_pad = self.lanes // 4 if (self.lanes >= 8 and fine and mean_run >= RUN_PAD_MIN_MEAN_RUN) else 0
+            self.tiles = corpus.vocab_tiles(rows, run_pad)
         self._reducer = None  # in-flight per-tile count all-reduces (draw -> resample)
         n_err = self.tiles.n_tiles if self.tiles is not None else 1
         self.err = torch.empty((n_err, 2), dtype=torch.int64, device=dev)

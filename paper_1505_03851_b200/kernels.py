@@ -182,11 +182,11 @@ class DeviceCorpus:
             raise ValueError("word lists shorter than the document lengths")
         return cls.from_csr(offsets, flat, doc_base, vocab_size)
 
-    def vocab_tiles(self, rows_per_tile: int) -> VocabTiles:
+    def vocab_tiles(self, rows_per_tile: int, run_pad: int = 0) -> VocabTiles:
         """Token list regrouped by vocabulary tile (cached per tile size)."""
-        key = ("tiles", int(rows_per_tile))
+        key = ("tiles", int(rows_per_tile), int(run_pad))
         if key not in self._last_key:
-            self._last_key[key] = _build_vocab_tiles(self, int(rows_per_tile))
+            self._last_key[key] = _build_vocab_tiles(self, int(rows_per_tile), int(run_pad))
         return self._last_key[key]
 
     def last_key(self, lanes: int):
@@ -211,6 +211,13 @@ class VocabTiles:
     theta rows stream; z, units and the hash keys still use each token's
     original (document, position), so results are bit-identical to the
     untiled draw.
+
+    run_pad > 0: every (tile, document) run of tokens is padded to a multiple
+    of run_pad slots (8 = the L consecutive chunk rows a lane group of the
+    butterfly kernel loads), so no lane group straddles two documents and
+    each lane needs ONE theta segment per block (no per-row selection).
+    Padding slots carry token_pos = -1, their run's document and its last
+    word: valid loads, nothing drawn.
     """
 
     words: object
@@ -218,24 +225,51 @@ class VocabTiles:
     token_pos: object
     bounds: list
     rows_per_tile: int
+    run_pad: int = 0
+    n_tokens: int = 0
 
     @property
     def n_tiles(self) -> int:
         return len(self.bounds) - 1
 
 
-def _build_vocab_tiles(corpus: "DeviceCorpus", rows_per_tile: int) -> VocabTiles:
+def _build_vocab_tiles(corpus: "DeviceCorpus", rows_per_tile: int, run_pad: int = 0) -> VocabTiles:
     torch = _torch()
     tile = torch.div(corpus.words, rows_per_tile, rounding_mode="floor").to(torch.int32)
     _, order = torch.sort(tile, stable=True)
     words = corpus.words[order].contiguous()
     doc = corpus.token_doc[order].contiguous()
     pos = (order - corpus.offsets[doc.long()]).to(torch.int32).contiguous()
+    tile = tile[order]
+    del order
     n_tiles = int(tile.max().item()) + 1 if corpus.n_tokens else 1
-    counts = torch.bincount(tile.long(), minlength=n_tiles).cpu().numpy()
+    T = corpus.n_tokens
+    if run_pad > 1 and T:
+        dev = words.device
+        brk = torch.ones(T, dtype=torch.bool, device=dev)
+        brk[1:] = (doc[1:] != doc[:-1]) | (tile[1:] != tile[:-1])
+        run_start = brk.nonzero().squeeze(1)
+        run_len = torch.diff(run_start, append=torch.tensor([T], device=dev))
+        plen = (run_len + run_pad - 1) // run_pad * run_pad
+        new_start = torch.cumsum(plen, 0) - plen
+        run_id = torch.cumsum(brk.to(torch.int64), 0) - 1
+        del brk
+        dest = new_start[run_id] + (torch.arange(T, device=dev) - run_start[run_id])
+        slot_run = torch.repeat_interleave(torch.arange(run_start.numel(), device=dev), plen)
+        pw = words[run_start + run_len - 1][slot_run]
+        pd = doc[run_start][slot_run]
+        pp = torch.full((slot_run.numel(),), -1, dtype=torch.int32, device=dev)
+        pw[dest] = words
+        pp[dest] = pos
+        counts = torch.zeros(n_tiles, dtype=torch.int64, device=dev).index_add_(0, tile[run_start].long(), plen)
+        counts = counts.cpu().numpy()
+        del dest, slot_run, run_id, new_start, run_start, run_len, plen
+        words, doc, pos = pw.contiguous(), pd.contiguous(), pp.contiguous()
+    else:
+        counts = torch.bincount(tile.long(), minlength=n_tiles).cpu().numpy()
     bounds = [0] + np.cumsum(counts).tolist()
-    del order, tile
-    return VocabTiles(words, doc, pos, [int(b) for b in bounds], int(rows_per_tile))
+    del tile
+    return VocabTiles(words, doc, pos, [int(b) for b in bounds], int(rows_per_tile), int(run_pad), int(T))
 
 
 def block_aligned_rows(n_rows: int, K: int, dtype=None, device=None, lanes: int = 32):

@@ -333,10 +333,12 @@ def test_full_size_rows_k1024_properties():
     np.testing.assert_array_equal(zbn[rows], exp)
 
 
+@pytest.mark.parametrize("run_pad", [0, 8])
 @pytest.mark.parametrize("kernel", ["butterfly", "transposed", "basic"])
-def test_vocab_tiled_draw_identical(kernel):
+def test_vocab_tiled_draw_identical(kernel, run_pad):
     """Drawing tile by tile over the vocabulary (phi slices L2-resident) gives
-    the same z and counts as the untiled draw, for every kernel and stop mode."""
+    the same z and counts as the untiled draw, for every kernel and stop mode,
+    with and without (tile, document) runs padded to the lane-group height."""
     gen = np.random.default_rng(11)
     M, V, K = 640, 1000, 128
     N, off, words = _random_corpus(gen, M, V, 40)
@@ -344,8 +346,14 @@ def test_vocab_tiled_draw_identical(kernel):
     phi = gen.uniform(0.05, 1, size=(V, K)).astype(np.float32)
     dc = wd.DeviceCorpus.from_csr(off, words.astype(np.int32))
     th, ph = _cuda(theta), _cuda(phi)
-    tiles = dc.vocab_tiles(137)
-    assert tiles.n_tiles == -(-V // 137) and tiles.bounds[-1] == dc.n_tokens
+    tiles = dc.vocab_tiles(137, run_pad)
+    assert tiles.n_tiles == -(-V // 137)
+    if run_pad:
+        pos = tiles.token_pos.cpu().numpy()
+        assert (pos >= 0).sum() == dc.n_tokens and tiles.bounds[-1] == pos.size > dc.n_tokens
+        assert all(b % run_pad == 0 for b in tiles.bounds)
+    else:
+        assert tiles.bounds[-1] == dc.n_tokens
     u = _cuda(gen.random(int(off[-1])))
     for stops in (wd.SeededStops(5), u):
         wt0 = torch.zeros((V, K), dtype=torch.int32, device="cuda")
@@ -404,9 +412,10 @@ def test_full_size_lda_k1024_sampled_tokens():
         assert idx == zs[j], (t, m, i)
 
 
+@pytest.mark.parametrize("run_pad", [0, 1])
 @pytest.mark.parametrize("K,W,dtype", [(4096, 32, np.float32), (200, 32, np.float32), (640, 8, np.float32),
                                        (320, 64, np.float32), (1024, 32, np.float64)])
-def test_lda_large_k_and_lanes_tiled_vs_oracle(K, W, dtype):
+def test_lda_large_k_and_lanes_tiled_vs_oracle(K, W, dtype, run_pad):
     """K up to 4096 (BASELINE configs[4] row length), other lane counts and
     float64, drawn through vocabulary tiles, against the oracle."""
     gen = np.random.default_rng(K + W)
@@ -415,7 +424,7 @@ def test_lda_large_k_and_lanes_tiled_vs_oracle(K, W, dtype):
     theta = gen.dirichlet(np.full(K, 0.1), size=M).astype(dtype)
     phi = gen.uniform(0.01, 1, size=(V, K)).astype(dtype)
     dc = wd.DeviceCorpus.from_csr(off, words.astype(np.int32))
-    tiles = dc.vocab_tiles(64)
+    tiles = dc.vocab_tiles(64, run_pad * W // 4)  # run_pad: the lane-group height W/4
     seed = 77
     z = wd.draw_z_device("butterfly", dc, _cuda(theta), _cuda(phi), wd.SeededStops(seed), W, tiles=tiles).cpu().numpy()
     exp, err = O.draw_z_csr(theta, phi, off, words, W=W, seed=seed, threads=8)

@@ -70,14 +70,14 @@ def timed(fn, n, warm=2):
     return a.elapsed_time(b) / 1e3 / n
 
 
-def run(name, peak):
+def run(name, peak, run_pad=None):
     M, V, K, mean, kind, iters = CONFIGS[name]
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(2026)
     off, words = make_corpus(M, V, mean, kind, g, dev)
     dc = wd.DeviceCorpus.from_csr(off, words, vocab_size=V)
     T = dc.n_tokens
-    lda = DeviceLDA(dc, K, V, seed=2026)
+    lda = DeviceLDA(dc, K, V, seed=2026, run_pad=run_pad)
     lda.init_uniform()
     it = [0]
 
@@ -99,6 +99,8 @@ def run(name, peak):
     res = {
         "config": name, "docs": dc.n_docs, "vocab": V, "topics": K, "tokens": T, "words": kind,
         "vocab_tiles": lda.tiles.n_tiles if lda.tiles is not None else 1,
+        "run_pad": lda.tiles.run_pad if lda.tiles is not None else 0,
+        "padded_slots": (lda.tiles.bounds[-1] - T) if lda.tiles is not None else 0,
         "iter_ms": t_iter * 1e3, "tokens_per_s_iter": T / t_iter,
         "draw_ms": t_draw * 1e3, "draw_tokens_per_s": T / t_draw,
         "draw_alg_gbs": T * bpt / t_draw / 1e9, "draw_alg_frac_hbm": T * bpt / t_draw / 1e9 / peak,
@@ -113,6 +115,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default=",".join(CONFIGS))
     ap.add_argument("--out", default="gpurun_out/configs.json")
+    ap.add_argument("--run-pad", type=int, default=None, help="force VocabTiles.run_pad (default: DeviceLDA's rule)")
     args = ap.parse_args()
     try:
         peak = float(json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -121,7 +124,7 @@ def main():
     out = []
     for name in args.only.split(","):
         t0 = time.time()
-        r = run(name, peak)
+        r = run(name, peak, args.run_pad)
         r["wall_s"] = time.time() - t0
         print(json.dumps(r), flush=True)
         out.append(r)

@@ -43,7 +43,8 @@ else:
     err = torch.empty(2, dtype=torch.int64, device="cuda")
     wt = torch.zeros((V, K), dtype=torch.int32, device="cuda")
     kern = "butterfly" if what in ("lda", "ldatiled") else "transposed"
-    tiles = dc.vocab_tiles((40 << 20) // (4 * K)) if what == "ldatiled" else None
+    run_pad = 8 if len(sys.argv) <= 4 else int(sys.argv[4])  # DeviceLDA's rule at K=1024
+    tiles = dc.vocab_tiles((40 << 20) // (4 * K), run_pad) if what == "ldatiled" else None
     err = torch.empty((tiles.n_tiles if tiles else 1, 2), dtype=torch.int64, device="cuda")
     for _ in range(4):
         wd.draw_z_device(kern, dc, theta, phi, wd.SeededStops(3), 32, z=z, err=err, word_topic=wt, check=False,
