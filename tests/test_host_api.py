@@ -143,3 +143,45 @@ def test_chi_square():
     stat, dof = wd.chi_square([10, 10], [0.5, 0.5])
     assert stat == 0.0 and dof == 1
     assert abs(wd.chi_square_critical(18) - 42.3124) < 1e-3
+
+
+@pytest.mark.parametrize("run_pad", [0, 8])
+def test_vocab_tile_builder_cpu(run_pad):
+    """The vocabulary-tile regrouping (plain torch ops, runs on CPU tensors):
+    every token appears exactly once with its (document, position); tiles
+    hold their word range in CSR order; with run_pad every (tile, document)
+    run starts and ends on a multiple of run_pad, padding slots carry
+    token_pos = -1 and their run's document."""
+    import torch
+
+    from paper_1505_03851_b200.kernels import DeviceCorpus, _build_vocab_tiles
+
+    gen = np.random.default_rng(5)
+    M, V, rows = 96, 70, 16
+    N = gen.poisson(9, size=M)
+    N[::7] = 0
+    off = np.concatenate([[0], np.cumsum(N)]).astype(np.int64)
+    words = gen.integers(0, V, size=int(off[-1])).astype(np.int32)
+    td = np.repeat(np.arange(M), N).astype(np.int32)
+    c = DeviceCorpus(torch.from_numpy(off), torch.from_numpy(words), torch.from_numpy(td), M, int(off[-1]))
+    t = _build_vocab_tiles(c, rows, run_pad)
+    w, d, p = t.words.numpy(), t.token_doc.numpy(), t.token_pos.numpy()
+    assert t.n_tiles == -(-int(words.max() + 1) // rows) and t.bounds[-1] == w.size
+    real = p >= 0
+    assert real.sum() == words.size
+    # each real slot is a distinct original token, with its word
+    orig = off[d[real]] + p[real]
+    assert np.array_equal(np.sort(orig), np.arange(words.size))
+    assert np.array_equal(w[real], words[orig])
+    for ti in range(t.n_tiles):
+        a, b = t.bounds[ti], t.bounds[ti + 1]
+        assert np.all(w[a:b] // rows == ti)
+        rr = real[a:b]
+        assert np.all(np.diff(orig[np.cumsum(real)[a:b][rr] - 1]) > 0)  # CSR order inside the tile
+        if run_pad:
+            assert (b - a) % run_pad == 0
+            dd = d[a:b]
+            starts = np.flatnonzero(np.r_[True, dd[1:] != dd[:-1]])
+            assert np.all(starts % run_pad == 0)
+    if not run_pad:
+        assert real.all()
