@@ -103,14 +103,21 @@ def main():
     z = torch.empty(T, dtype=torch.int32, device="cuda")
     lda = []
     for K in [int(x) for x in a.lda_ks.split(",")]:
-        theta = torch.rand((M, K), generator=g, device="cuda") * 0.9 + 0.1
-        phi = torch.rand((V, K), generator=g, device="cuda") * 0.9 + 0.1
+        # the product's layout (DeviceLDA): line-aligned theta/phi blocks,
+        # vocabulary tiles when phi exceeds ~40 MB, and for the butterfly
+        # kernel (tile, document) runs padded to 8 when they are long
+        theta = wd.kernels.to_block_aligned(torch.rand((M, K), generator=g, device="cuda") * 0.9 + 0.1)
+        phi = wd.kernels.to_block_aligned(torch.rand((V, K), generator=g, device="cuda") * 0.9 + 0.1)
         r = {"K": K}
-        # the product's default: vocabulary tiles when phi exceeds ~40 MB (DeviceLDA)
-        tiles = dc.vocab_tiles((40 << 20) // (4 * K)) if V * K * 4 > (40 << 20) else None
-        r["vocab_tiles"] = tiles.n_tiles if tiles else 1
-        terr = torch.empty((r["vocab_tiles"], 2), dtype=torch.int64, device="cuda")
+        rows_t = (40 << 20) // (4 * K)
+        tiled = V * K * 4 > (40 << 20)
+        n_tiles = -(-V // rows_t) if tiled else 1
+        pad = 8 if (tiled and K // 32 <= 32 and T / M / n_tiles >= 20) else 0
+        r["vocab_tiles"] = n_tiles
+        r["run_pad"] = pad
+        terr = torch.empty((n_tiles, 2), dtype=torch.int64, device="cuda")
         for kern in ("butterfly", "transposed"):
+            tiles = dc.vocab_tiles(rows_t, pad if kern == "butterfly" else 0) if tiled else None
             dt = timed(lambda: wd.draw_z_device(kern, dc, theta, phi, wd.SeededStops(3), 32, z=z, err=terr,
                                                 check=False, tiles=tiles), flush, iters=5, warm=2)
             r[kern] = {"ms": dt * 1e3, "tokens_per_s": T / dt,
