@@ -328,55 +328,22 @@ def main():
     # static across iterations and stays resident (uploaded once per Corpus).
     e2e = None
     if not args.no_e2e:
-        # Inputs of step s+1 are copied (pinned H2D, copy stream) while step s
-        # computes, and z of step s returns (D2H, second copy stream) while
-        # step s+1 computes: the prefetching a data loader does.  Every step
-        # still moves its full inputs and result across PCIe.
+        # DeviceLDA.iterate_from_host: inputs of step s+1 are copied (pinned
+        # H2D, copy stream) while step s computes, and z of step s returns
+        # (D2H, second copy stream) while step s+1 computes: the prefetching
+        # a data loader does.  Every step moves its full inputs and result.
         h_theta = lda.theta.cpu().pin_memory()
         h_phi = lda.phi.cpu().pin_memory()
         h_z = torch.empty(n_tok, dtype=torch.int32).pin_memory()
         h2d = h_theta.numel() * h_theta.element_size() + h_phi.numel() * h_phi.element_size()
         d2h = n_tok * 4
-        from paper_1505_03851_b200.kernels import block_aligned_rows
-
-        th_buf = [lda.theta, block_aligned_rows(*lda.theta.shape, lda.theta.dtype, dev)]
-        ph_buf = [lda.phi, block_aligned_rows(*lda.phi.shape, lda.phi.dtype, dev)]
-        z_buf = [lda.z, torch.empty_like(lda.z)]
-        up, down = torch.cuda.Stream(), torch.cuda.Stream()
-        ready = [torch.cuda.Event() for _ in range(2)]
-        done = [torch.cuda.Event() for _ in range(2)]
-
-        def upload(i):
-            up.wait_event(done[i])  # buffer i free (its last iteration finished)
-            with torch.cuda.stream(up):
-                th_buf[i].copy_(h_theta, non_blocking=True)
-                ph_buf[i].copy_(h_phi, non_blocking=True)
-                ready[i].record(up)
-
-        def run(n, t0):
-            for i in range(2):
-                done[i].record(stream)
-            upload(0)
-            for s in range(n):
-                i = s % 2
-                if s + 1 < n:
-                    upload(1 - i)
-                stream.wait_event(ready[i])
-                lda.theta, lda.phi, lda.z = th_buf[i], ph_buf[i], z_buf[i]
-                lda.iterate(t0 + s)
-                done[i].record(stream)
-                down.wait_event(done[i])
-                with torch.cuda.stream(down):
-                    h_z.copy_(z_buf[i], non_blocking=True)
-            stream.wait_stream(down)
-
-        run(2, 100)
+        lda.iterate_from_host(100, 2, h_theta, h_phi, h_z)  # warm-up (buffers, streams)
         torch.cuda.synchronize()
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n_e2e = max(3, min(args.steps, 6))
         a.record(stream)
-        run(n_e2e, 200)
+        lda.iterate_from_host(200, n_e2e, h_theta, h_phi, h_z)
         b.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -386,10 +353,10 @@ def main():
         lda.check_errors()
         e2e = {"value": total_tokens / float(et[0]), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(et[0]) * 1e3,
-               "path": "pinned host theta/phi -> Gibbs iteration on the resident corpus -> z to host "
-                       "(next step's H2D and previous step's D2H overlap the current step)"}
-        lda.theta, lda.phi, lda.z = th_buf[0], ph_buf[0], z_buf[0]
-        del h_theta, h_phi, h_z, th_buf, ph_buf, z_buf
+               "path": "DeviceLDA.iterate_from_host: pinned host theta/phi -> Gibbs iteration on the resident "
+                       "corpus -> z to host (next step's H2D and previous step's D2H overlap the current step)"}
+        del h_theta, h_phi, h_z
+        lda._host_pipe = None
 
     # ------------------------------------------- standalone sampler (configs[1])
     sampler = None

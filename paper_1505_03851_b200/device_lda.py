@@ -158,6 +158,59 @@ class DeviceLDA:
         self.allreduce_counts()
         self.resample(t)
 
+    def iterate_from_host(self, t0: int, n: int, theta_host, phi_host, z_host=None):
+        """n iterations, each ENTERED FROM HOST parameters: the drop-in
+        gibbs_iterate(corpus, params, ...) call made with host theta/phi
+        (pinned torch tensors) every iteration, z of each iteration returned
+        to z_host (pinned int32 [n_tokens]).  Every iteration moves its full
+        inputs and result across PCIe; the copies are pipelined the way a
+        data loader prefetches: iteration s+1's H2D (copy stream) and
+        iteration s-1's D2H (second copy stream) overlap iteration s, on two
+        device buffer sets.  Stream-ordered: returns without synchronising
+        (the current stream waits for the last D2H)."""
+        torch = self.torch
+        st = torch.cuda.current_stream()
+        if getattr(self, "_host_pipe", None) is None:
+            self._host_pipe = {
+                "theta": [self.theta, block_aligned_rows(*self.theta.shape, self.theta.dtype, self.device, self.lanes)],
+                "phi": [self.phi, block_aligned_rows(*self.phi.shape, self.phi.dtype, self.device, self.lanes)],
+                "z": [self.z, torch.empty_like(self.z)],
+                "up": torch.cuda.Stream(), "down": torch.cuda.Stream(),
+                "ready": [torch.cuda.Event() for _ in range(2)],
+                "done": [torch.cuda.Event() for _ in range(2)],
+                "copied": [torch.cuda.Event() for _ in range(2)],
+            }
+        P = self._host_pipe
+        up, down = P["up"], P["down"]
+        for i in range(2):
+            P["done"][i].record(st)
+            P["copied"][i].record(st)
+
+        def upload(i):
+            up.wait_event(P["done"][i])  # buffer set i free: its last iteration finished
+            with torch.cuda.stream(up):
+                P["theta"][i].copy_(theta_host, non_blocking=True)
+                P["phi"][i].copy_(phi_host, non_blocking=True)
+                P["ready"][i].record(up)
+
+        if n > 0:
+            upload(0)
+        for s in range(n):
+            i = s % 2
+            if s + 1 < n:
+                upload(1 - i)
+            st.wait_event(P["ready"][i])
+            st.wait_event(P["copied"][i])  # z buffer i's previous D2H has drained
+            self.theta, self.phi, self.z = P["theta"][i], P["phi"][i], P["z"][i]
+            self.iterate(t0 + s)
+            P["done"][i].record(st)
+            if z_host is not None:
+                down.wait_event(P["done"][i])
+                with torch.cuda.stream(down):
+                    z_host.copy_(P["z"][i], non_blocking=True)
+                    P["copied"][i].record(down)
+        st.wait_stream(down)
+
     def check_errors(self):
         raise_for_err(combine_err(self.err), _lib.WD_KEYS_MASTER, self.lanes)
 

@@ -149,3 +149,29 @@ def test_sampler_chi_square():
     draws = wd.sample_butterfly(weights, 1_000_000, seed=61)
     stat, dof = wd.chi_square(np.bincount(draws, minlength=19), weights / weights.sum())
     assert dof == 18 and stat < wd.chi_square_critical(18, 0.001)
+
+
+def test_iterate_from_host_matches_resident_iterations():
+    """DeviceLDA.iterate_from_host (the e2e path of bench.py): every iteration
+    re-enters from the same host theta/phi, so iteration t's z must equal a
+    resident iterate(t) started from those parameters; pipelining (two buffer
+    sets, copy streams) must not change any bit."""
+    gen = np.random.default_rng(21)
+    M, V, K = 320, 600, 96
+    off, words = _corpus(gen, M, V, 30)
+    dc = wd.DeviceCorpus.from_csr(off, words)
+    lda = DeviceLDA(dc, K, V, seed=4)
+    lda.init_uniform()
+    h_theta = lda.theta.cpu().pin_memory()
+    h_phi = lda.phi.cpu().pin_memory()
+    h_z = torch.empty(dc.n_tokens, dtype=torch.int32).pin_memory()
+    lda.iterate_from_host(10, 3, h_theta, h_phi, h_z)
+    torch.cuda.synchronize()
+    lda.check_errors()
+    ref = DeviceLDA(dc, K, V, seed=4)
+    ref.theta.copy_(h_theta)
+    ref.phi.copy_(h_phi)
+    ref.iterate(12)  # the last of the three
+    np.testing.assert_array_equal(h_z.numpy(), ref.z.cpu().numpy())
+    np.testing.assert_array_equal(lda.theta.cpu().numpy(), ref.theta.cpu().numpy())
+    np.testing.assert_array_equal(lda.phi.cpu().numpy(), ref.phi.cpu().numpy())
