@@ -41,6 +41,9 @@ enum { MODE_LDA = 0, MODE_ROWS = 1 };
 #ifndef WD_LDA_MIN_BLOCKS
 #define WD_LDA_MIN_BLOCKS 6
 #endif
+#ifndef WD_LDA_MIN_BLOCKS_F64  // float64 LDA draw (unbounded: 237 registers, 8 warps/SM)
+#define WD_LDA_MIN_BLOCKS_F64 4  // measured (cfg4 fp64 draw): unbounded 419 ms, 3 -> 156, 4 -> 153, 5 -> 155, 6 -> 236
+#endif
 #ifndef WD_LDA_MIN_BLOCKS_COARSE  // K > 32 * W: the group recompute needs more registers
                                    // (measured at K = 4096: 4 -> 463 ms, 5 -> 415, 6 -> 468 per cfg5 draw)
 #define WD_LDA_MIN_BLOCKS_COARSE 5
@@ -469,7 +472,9 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
                                                           : (MODE == MODE_LDA ? (COARSE ? WD_LDA_MIN_BLOCKS_COARSE
                                                                                         : WD_LDA_MIN_BLOCKS)
                                                                               : 8))
-                                             : 1)
+                                             : ((sizeof(T) == 8 && W == 32 && VEC && MODE == MODE_LDA)
+                                                    ? WD_LDA_MIN_BLOCKS_F64
+                                                    : 1))
     bfly_kernel(DrawParams<T> p) {
   using GW = Geo<W>;
   constexpr int E = GW::E, L = GW::L, R = GW::R;
