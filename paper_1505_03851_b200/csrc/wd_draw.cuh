@@ -44,6 +44,9 @@ enum { MODE_LDA = 0, MODE_ROWS = 1 };
 #ifndef WD_LDA_MIN_BLOCKS_F64  // float64 LDA draw (unbounded: 237 registers, 8 warps/SM)
 #define WD_LDA_MIN_BLOCKS_F64 4  // measured (cfg4 fp64 draw): unbounded 419 ms, 3 -> 156, 4 -> 153, 5 -> 155, 6 -> 236
 #endif
+#ifndef WD_MIN_BLOCKS_OTHER  // vector path, W != 32 or float64 rows
+#define WD_MIN_BLOCKS_OTHER 4
+#endif
 #ifndef WD_LDA_MIN_BLOCKS_COARSE  // K > 32 * W: the group recompute needs more registers
                                    // (measured at K = 4096: 4 -> 463 ms, 5 -> 415, 6 -> 468 per cfg5 draw)
 #define WD_LDA_MIN_BLOCKS_COARSE 5
@@ -466,15 +469,20 @@ template <typename T> struct Walk<T, 0> {
   static __device__ __forceinline__ void run(T*, T&, T&, T, int, int&) {}
 };
 
+// Minimum resident CTAs per SM (register cap) of each bfly_kernel instantiation.
 template <typename T, int W, bool VEC, int MODE, int PIPE, bool COARSE>
-__global__ void __launch_bounds__(128, (sizeof(T) == 4 && W == 32 && VEC)
-                                             ? (PIPE == 2 ? 4
-                                                          : (MODE == MODE_LDA ? (COARSE ? WD_LDA_MIN_BLOCKS_COARSE
-                                                                                        : WD_LDA_MIN_BLOCKS)
-                                                                              : 8))
-                                             : ((sizeof(T) == 8 && W == 32 && VEC && MODE == MODE_LDA)
-                                                    ? WD_LDA_MIN_BLOCKS_F64
-                                                    : 1))
+constexpr int bfly_min_blocks() {
+  if (sizeof(T) == 4 && W == 32 && VEC)
+    return PIPE == 2 ? 4 : (MODE == MODE_LDA ? (COARSE ? WD_LDA_MIN_BLOCKS_COARSE : WD_LDA_MIN_BLOCKS) : 8);
+  if (sizeof(T) == 8 && W == 32 && VEC && MODE == MODE_LDA) return WD_LDA_MIN_BLOCKS_F64;
+  // other lane counts: uncapped they take 150-250 registers (float64 W = 64
+  // would spill at 4 CTAs)
+  if (VEC) return (sizeof(T) == 8 && W == 64) ? 2 : WD_MIN_BLOCKS_OTHER;
+  return 1;
+}
+
+template <typename T, int W, bool VEC, int MODE, int PIPE, bool COARSE>
+__global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, COARSE>()))
     bfly_kernel(DrawParams<T> p) {
   using GW = Geo<W>;
   constexpr int E = GW::E, L = GW::L, R = GW::R;

@@ -70,14 +70,14 @@ def timed(fn, n, warm=2):
     return a.elapsed_time(b) / 1e3 / n
 
 
-def run(name, peak, run_pad=None, dtype="float32"):
+def run(name, peak, run_pad=None, dtype="float32", lanes=32):
     M, V, K, mean, kind, iters = CONFIGS[name]
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(2026)
     off, words = make_corpus(M, V, mean, kind, g, dev)
     dc = wd.DeviceCorpus.from_csr(off, words, vocab_size=V)
     T = dc.n_tokens
-    lda = DeviceLDA(dc, K, V, seed=2026, run_pad=run_pad, dtype=getattr(torch, dtype))
+    lda = DeviceLDA(dc, K, V, seed=2026, run_pad=run_pad, dtype=getattr(torch, dtype), lanes=lanes)
     lda.init_uniform()
     it = [0]
 
@@ -98,7 +98,7 @@ def run(name, peak, run_pad=None, dtype="float32"):
     if kind == "zipf":
         top_share = float((words == 0).sum().item()) / T
     res = {
-        "config": name, "dtype": dtype, "docs": dc.n_docs, "vocab": V, "topics": K, "tokens": T, "words": kind,
+        "config": name, "dtype": dtype, "lanes": lanes, "docs": dc.n_docs, "vocab": V, "topics": K, "tokens": T, "words": kind,
         "vocab_tiles": lda.tiles.n_tiles if lda.tiles is not None else 1,
         "run_pad": lda.tiles.run_pad if lda.tiles is not None else 0,
         "padded_slots": (lda.tiles.bounds[-1] - T) if lda.tiles is not None else 0,
@@ -118,6 +118,7 @@ def main():
     ap.add_argument("--out", default="gpurun_out/configs.json")
     ap.add_argument("--run-pad", type=int, default=None, help="force VocabTiles.run_pad (default: DeviceLDA's rule)")
     ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
+    ap.add_argument("--lanes", type=int, default=32)
     args = ap.parse_args()
     try:
         peak = float(json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -126,7 +127,7 @@ def main():
     out = []
     for name in args.only.split(","):
         t0 = time.time()
-        r = run(name, peak, args.run_pad, args.dtype)
+        r = run(name, peak, args.run_pad, args.dtype, args.lanes)
         r["wall_s"] = time.time() - t0
         print(json.dumps(r), flush=True)
         out.append(r)
