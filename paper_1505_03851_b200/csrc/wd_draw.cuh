@@ -469,9 +469,21 @@ template <typename T> struct Walk<T, 0> {
   static __device__ __forceinline__ void run(T*, T&, T&, T, int, int&) {}
 };
 
+// Elements of the per-warp running-sum array S: nbc blocks x 32 lanes, at
+// least a [32][TS] tile when the cooperative pass-2 reload uses S as its tile
+// (no remnant tile).  Shared by the kernel and the launcher.
+__host__ __device__ constexpr int bfly_s_elems(int nbc, int rem, int TS, bool coop) {
+  return (coop && rem == 0 && nbc * 32 < 32 * TS) ? 32 * TS : nbc * 32;
+}
+
 // Minimum resident CTAs per SM (register cap) of each bfly_kernel instantiation.
-template <typename T, int W, bool VEC, int MODE, int PIPE, bool COARSE>
+// KV (K variant) of a bfly_kernel instantiation: which block-sum storage and
+// pass-2 reload it compiles (chosen per launch from nb = K / W).
+enum { KV_FINE = 0, KV_COARSE = 1, KV_SMALL = 2 };
+
+template <typename T, int W, bool VEC, int MODE, int PIPE, int KV>
 constexpr int bfly_min_blocks() {
+  constexpr bool COARSE = KV == KV_COARSE;
   if (sizeof(T) == 4 && W == 32 && VEC)
     return PIPE == 2 ? 4 : (MODE == MODE_LDA ? (COARSE ? WD_LDA_MIN_BLOCKS_COARSE : WD_LDA_MIN_BLOCKS) : 8);
   if (sizeof(T) == 8 && W == 32 && VEC && MODE == MODE_LDA) return WD_LDA_MIN_BLOCKS_F64;
@@ -481,9 +493,12 @@ constexpr int bfly_min_blocks() {
   return 1;
 }
 
-template <typename T, int W, bool VEC, int MODE, int PIPE, bool COARSE>
-__global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, COARSE>()))
+template <typename T, int W, bool VEC, int MODE, int PIPE, int KV>
+__global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, KV>()))
     bfly_kernel(DrawParams<T> p) {
+  // KV_COARSE: more than 32 blocks per row, every G-th running sum kept;
+  // KV_SMALL (LDA, vector, at most 16 blocks): warp-cooperative pass-2 reload
+  constexpr bool COARSE = KV == KV_COARSE;
   using GW = Geo<W>;
   constexpr int E = GW::E, L = GW::L, R = GW::R;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -495,15 +510,19 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, C
   const int G = COARSE ? (nb > 32 ? (nb + 31) / 32 : 1) : 1;
   const int nbc = nb > 0 ? (nb + G - 1) / G : 1;
   const int wpb_i = blockDim.x >> 5;
-  T* S = reinterpret_cast<T*>(smem_raw) + (size_t)wib * (size_t)nbc * 32;
   // remnant tile [32 rows][TS] per warp (after every warp's S).  Vector path:
   // stride W + 4 keeps rows 16-byte aligned and the 128-bit segment stores /
   // row scans conflict-free; scalar path: odd stride W + 1.
   constexpr int TS = VEC ? W + 4 : W + 1;
-  T* RT = reinterpret_cast<T*>(smem_raw) + (size_t)wpb_i * (size_t)nbc * 32 + (size_t)wib * 32 * TS;
+  // warp-cooperative pass-2 reload (LDA, vector, fine): with no remnant tile
+  // the reload tile aliases S, which is then sized for it
+  constexpr bool COOP = MODE == MODE_LDA && VEC && KV == KV_SMALL;
+  const size_t SW = (size_t)bfly_s_elems(nbc, rem, TS, COOP);  // S elements per warp
+  T* S = reinterpret_cast<T*>(smem_raw) + (size_t)wib * SW;
+  T* RT = reinterpret_cast<T*>(smem_raw) + (size_t)wpb_i * SW + (size_t)wib * 32 * TS;
   // cp.async ring (PIPE 5/6), after every warp's S and remnant tile
   constexpr bool RING = PIPE >= 5;
-  char* ring = reinterpret_cast<char*>(reinterpret_cast<T*>(smem_raw) + (size_t)wpb_i * (size_t)nbc * 32 +
+  char* ring = reinterpret_cast<char*>(reinterpret_cast<T*>(smem_raw) + (size_t)wpb_i * SW +
                                        (size_t)wpb_i * 32 * TS) +
                (size_t)wib * RingDepth<PIPE>::NS * RingStage<W>::BYTES;
   const int s = lane % L;
@@ -721,20 +740,111 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, C
     __syncwarp();
     const T total = acc;
 
-    if (own_valid) {
-      uint64_t ka, kb;
-      unsigned long long ekey;
-      int r;
-      int64_t zidx;
-      token_keys<T, MODE>(p, own_tok, own_doc, W, ka, kb, ekey, r, zidx);
-      const T stop = make_stop<T>(p, zidx, total, ka, kb, MODE == MODE_ROWS);
-      if (!(total > T(0))) atomicMin(p.err, ekey);
-      // block bisection over S (kernels.py:337-346): the first block whose
-      // running sum exceeds stop (S is nondecreasing, so any search that finds
-      // that block is the reference's bisection)
+    if constexpr (!COOP) {
+      // per-lane pass 2 (kept verbatim for the fine and coarse variants:
+      // their register allocation is tuned)
+      if (own_valid) {
+        uint64_t ka, kb;
+        unsigned long long ekey;
+        int r;
+        int64_t zidx;
+        token_keys<T, MODE>(p, own_tok, own_doc, W, ka, kb, ekey, r, zidx);
+        const T stop = make_stop<T>(p, zidx, total, ka, kb, MODE == MODE_ROWS);
+        if (!(total > T(0))) atomicMin(p.err, ekey);
+        // block bisection over S (kernels.py:337-346): the first block whose
+        // running sum exceeds stop (S is nondecreasing, so any search that finds
+        // that block is the reference's bisection)
+        T cur[W];
+        int j;
+        T prev, high;
+        auto load_block = [&](int64_t base) {  // own row's products of one block
+          constexpr int NG = W / E;
+          constexpr int HG = NG >= 4 ? NG / 2 : NG;
+#pragma unroll
+          for (int h = 0; h < NG; h += HG) {
+#pragma unroll
+            for (int g = h; g < h + HG; ++g) {
+              Seg<T, E, VEC> x;
+              x.load(pown + base + g * E);
+              if (MODE == MODE_LDA) {
+                Seg<T, E, VEC> th;
+                th.load(town + base + g * E);
+#pragma unroll
+                for (int e = 0; e < E; ++e) cur[g * E + e] = mul_rn(th.v[e], x.v[e]);
+              } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) cur[g * E + e] = x.v[e];
+              }
+            }
+          }
+        };
+        {
+          int lo2 = 0, hi2 = nbc - 1;
+          while (lo2 < hi2) {
+            const int mid = (lo2 + hi2) >> 1;
+            if (stop < S[mid * 32 + lane]) hi2 = mid; else lo2 = mid + 1;
+          }
+          if (!COARSE || G == 1) {
+            j = lo2;
+            prev = j > 0 ? S[(j - 1) * 32 + lane] : prem;
+            high = nb > 0 ? S[j * 32 + lane] : T(0);
+          } else {
+            // recompute the selected group's block totals and running sums
+            T run = lo2 > 0 ? S[(lo2 - 1) * 32 + lane] : prem;
+            const int b0 = lo2 * G, b1 = min(b0 + G, nb);
+            j = b1 - 1;
+            prev = run;
+            high = run;
+            for (int bj = b0; bj < b1; ++bj) {
+              load_block((int64_t)rem + (int64_t)bj * W);
+              const T sb = add_rn(run, Tree<T, W>::sum(cur));
+              if (stop < sb || bj == b1 - 1) {
+                j = bj;
+                prev = run;
+                high = sb;
+                break;
+              }
+              run = sb;
+            }
+          }
+        }
+        const int64_t bb = (int64_t)rem + (int64_t)j * W;
+        if (bb == 0) prev = T(0);
+        const bool fallback = bb > 0 && stop < prev && total > T(0);
+        int result = 0;
+        if (nb > 0 && !fallback) {
+          // rebuild the selected block's products (own row) and walk it
+          load_block(bb);  // coarse: reloaded (L1 hit) rather than kept live, which
+                           // lets the coarse kernel fit 5 CTAs per SM
+          T low = prev;
+          int lo = 0;
+          Walk<T, W / 2>::run(cur, low, high, stop, r, lo);
+          result = (int)bb + lo;
+        }
+        if (fallback) {
+          // linear remnant fallback (kernels.py:354-361), products from the tile(s)
+          T a2 = T(0);
+          for (int t = 0; t < rem; ++t) {
+            const T a = (MODE == MODE_LDA && async_rem) ? mul_rn(__ldg(town + t), RT[own * TS + t]) : RT[own * TS + t];
+            a2 = add_rn(a2, a);
+            if (stop < a2) { result = t; break; }
+          }
+        }
+        p.z[zidx] = result;
+        if (MODE == MODE_LDA) {
+          if (p.word_topic) atomicAdd(p.word_topic + (int64_t)own_word * K + result, 1);
+          if (p.doc_topic) atomicAdd(p.doc_topic + (int64_t)own_doc * K + result, 1);
+        }
+      }
+    } else {
+      // ---- pass 2a (per lane): keys, stop, block bisection over S
+      uint64_t ka = 0, kb = 0;
+      unsigned long long ekey = 0;
+      int r = 0;
+      int64_t zidx = 0;
+      T stop = T(0), prev = T(0), high = T(0);
+      int j = 0;
       T cur[W];
-      int j;
-      T prev, high;
       auto load_block = [&](int64_t base) {  // own row's products of one block
         constexpr int NG = W / E;
         constexpr int HG = NG >= 4 ? NG / 2 : NG;
@@ -756,7 +866,13 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, C
           }
         }
       };
-      {
+      if (own_valid) {
+        token_keys<T, MODE>(p, own_tok, own_doc, W, ka, kb, ekey, r, zidx);
+        stop = make_stop<T>(p, zidx, total, ka, kb, MODE == MODE_ROWS);
+        if (!(total > T(0))) atomicMin(p.err, ekey);
+        // block bisection over S (kernels.py:337-346): the first block whose
+        // running sum exceeds stop (S is nondecreasing, so any search that finds
+        // that block is the reference's bisection)
         int lo2 = 0, hi2 = nbc - 1;
         while (lo2 < hi2) {
           const int mid = (lo2 + hi2) >> 1;
@@ -788,30 +904,73 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, C
       }
       const int64_t bb = (int64_t)rem + (int64_t)j * W;
       if (bb == 0) prev = T(0);
-      const bool fallback = bb > 0 && stop < prev && total > T(0);
-      int result = 0;
-      if (nb > 0 && !fallback) {
-        // rebuild the selected block's products (own row) and walk it
-        load_block(bb);  // coarse: reloaded (L1 hit) rather than kept live, which
-                         // lets the coarse kernel fit 5 CTAs per SM
-        T low = prev;
-        int lo = 0;
-        Walk<T, W / 2>::run(cur, low, high, stop, r, lo);
-        result = (int)bb + lo;
-      }
-      if (fallback) {
-        // linear remnant fallback (kernels.py:354-361), products from the tile(s)
-        T a2 = T(0);
-        for (int t = 0; t < rem; ++t) {
-          const T a = (MODE == MODE_LDA && async_rem) ? mul_rn(__ldg(town + t), RT[own * TS + t]) : RT[own * TS + t];
-          a2 = add_rn(a2, a);
-          if (stop < a2) { result = t; break; }
+      const bool fallback = own_valid && bb > 0 && stop < prev && total > T(0);
+      const bool walk = own_valid && nb > 0 && !fallback;
+
+      // ---- pass 2b: the selected block's products of the own row
+      {
+        // Warp-cooperative reload: lane group rg fetches target lane t's block
+        // segment (one 128-byte row segment per group per instruction, the
+        // coalesced pattern of pass 1) into t's row of a shared tile, instead
+        // of every lane gathering its own 32 values from 32 different lines
+        // per instruction (~31 L1 tag requests each, the largest tag-request
+        // source at small K).  The tile is the remnant tile (rows of walking
+        // lanes only; a fallback lane's remnant row is left intact) or, with
+        // no remnant, S (free once every lane has read its bounds).
+        T* tile = rem > 0 ? RT : S;
+        __syncwarp();
+        const uint32_t wmask = __ballot_sync(FULL, walk);
+        const int bbi = (int)bb;
+#pragma unroll
+        for (int i = 0; i < 32 / R; ++i) {
+          const int t = i * R + rg;
+          const int32_t wt = __shfl_sync(FULL, own_word, t);
+          const int32_t dt = __shfl_sync(FULL, own_doc, t);
+          const int bt = __shfl_sync(FULL, bbi, t);
+          if ((wmask >> t) & 1u) {
+            Seg<T, E, VEC> x, th;
+            x.load(p.phi + (int64_t)wt * p.ld_phi + bt + s * E);
+            th.load(p.theta + (int64_t)dt * p.ld_theta + bt + s * E);
+            T a[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) a[e] = mul_rn(th.v[e], x.v[e]);
+            store_seg(tile + t * TS + s * E, a);
+          }
+        }
+        __syncwarp();
+        if (walk) {
+#pragma unroll
+          for (int g = 0; g < W / E; ++g) {
+            T a[E];
+            load_seg_smem(a, tile + lane * TS + g * E);
+#pragma unroll
+            for (int e = 0; e < E; ++e) cur[g * E + e] = a[e];
+          }
         }
       }
-      p.z[zidx] = result;
-      if (MODE == MODE_LDA) {
-        if (p.word_topic) atomicAdd(p.word_topic + (int64_t)own_word * K + result, 1);
-        if (p.doc_topic) atomicAdd(p.doc_topic + (int64_t)own_doc * K + result, 1);
+
+      if (own_valid) {
+        int result = 0;
+        if (walk) {
+          T low = prev;
+          int lo = 0;
+          Walk<T, W / 2>::run(cur, low, high, stop, r, lo);
+          result = (int)bb + lo;
+        }
+        if (fallback) {
+          // linear remnant fallback (kernels.py:354-361), products from the tile(s)
+          T a2 = T(0);
+          for (int t = 0; t < rem; ++t) {
+            const T a = (MODE == MODE_LDA && async_rem) ? mul_rn(__ldg(town + t), RT[own * TS + t]) : RT[own * TS + t];
+            a2 = add_rn(a2, a);
+            if (stop < a2) { result = t; break; }
+          }
+        }
+        p.z[zidx] = result;
+        if (MODE == MODE_LDA) {
+          if (p.word_topic) atomicAdd(p.word_topic + (int64_t)own_word * K + result, 1);
+          if (p.doc_topic) atomicAdd(p.doc_topic + (int64_t)own_doc * K + result, 1);
+        }
       }
     }
     __syncwarp();

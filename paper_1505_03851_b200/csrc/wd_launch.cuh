@@ -39,14 +39,17 @@ inline int occupancy_blocks(const void* fn, size_t smem, int threads = kThreads)
   return nb;
 }
 
-// shared memory of one warp: running block sums S[b][lane] + remnant tile
+// shared memory of one warp: running block sums S[b][lane] (sized for the
+// cooperative reload tile when that aliases S) + remnant tile + cp.async ring
 template <typename T>
-inline size_t bfly_smem_per_warp(int W, int K, int mode, int pipe = 1) {
+inline size_t bfly_smem_per_warp(int W, int K, int mode, int pipe, bool vec, int kv) {
   int nb = K / W;
-  int G = nb > 32 ? (nb + 31) / 32 : 1;  // coarse running sums (bfly_kernel)
+  int G = (kv == KV_COARSE && nb > 32) ? (nb + 31) / 32 : 1;  // coarse running sums (bfly_kernel)
   int nbc = nb > 0 ? (nb + G - 1) / G : 1;
-  size_t b = (size_t)nbc * 32 * sizeof(T);
-  if (K % W || pipe >= 5) b += (size_t)32 * (W + 4) * sizeof(T);  // remnant tile (the ring sits after it)
+  const int TS = vec ? W + 4 : W + 1;
+  const bool coop = mode == MODE_LDA && vec && kv == KV_SMALL;
+  size_t b = (size_t)bfly_s_elems(nbc, K % W, TS, coop) * sizeof(T);
+  if (K % W || pipe >= 5) b += (size_t)32 * TS * sizeof(T);  // remnant tile (the ring sits after it)
   if (pipe >= 5) b += (size_t)(pipe == 6 ? 4 : 3) * ((W >= 4 ? W / 4 : 1) + 2) * 32 * 16;  // cp.async ring
   return b;
 }
@@ -79,10 +82,10 @@ inline void l2_policies(int mode, int& px, int& pt) {
   pt = lt >= 0 ? lt : 0;
 }
 
-template <typename T, int W, bool VEC, int MODE, int PIPE, bool COARSE>
+template <typename T, int W, bool VEC, int MODE, int PIPE, int KV>
 int launch_bfly_pc(const DrawParams<T>& p, cudaStream_t st) {
-  const void* fn = (const void*)bfly_kernel<T, W, VEC, MODE, PIPE, COARSE>;
-  const size_t per_warp = bfly_smem_per_warp<T>(W, p.K, MODE, PIPE);
+  const void* fn = (const void*)bfly_kernel<T, W, VEC, MODE, PIPE, KV>;
+  const size_t per_warp = bfly_smem_per_warp<T>(W, p.K, MODE, PIPE, VEC, KV);
   int wpb = kThreads / 32;  // fewer warps per CTA when the block sums are large
   while (wpb > 1 && (size_t)wpb * per_warp > 227 * 1024) wpb >>= 1;
   const size_t smem = (size_t)wpb * per_warp;
@@ -95,17 +98,25 @@ int launch_bfly_pc(const DrawParams<T>& p, cudaStream_t st) {
   int64_t cap = (int64_t)per_sm * device_sm_count();
   int grid = (int)(want < cap ? want : cap);
   if (grid <= 0) return WD_OK;
-  bfly_kernel<T, W, VEC, MODE, PIPE, COARSE><<<grid, threads, smem, st>>>(p);
+  bfly_kernel<T, W, VEC, MODE, PIPE, KV><<<grid, threads, smem, st>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { set_last_cuda_error(e); return WD_ERR_CUDA; }
   return WD_OK;
 }
 
-// more than 32 blocks per row: the coarse-running-sum instantiation
+// K variant: more than 32 blocks per row -> coarse running sums; LDA vector
+// path with at most 16 blocks -> the cooperative pass-2 reload (measured:
+// K = 200 draw -3.5%; at K = 1024 it cost +6%, so larger K keep the per-lane
+// reload)
+constexpr int kSmallMaxBlocks = 16;
 template <typename T, int W, bool VEC, int MODE, int PIPE>
 int launch_bfly_pipe(const DrawParams<T>& p, cudaStream_t st) {
-  if (p.K / W > 32) return launch_bfly_pc<T, W, VEC, MODE, PIPE, true>(p, st);
-  return launch_bfly_pc<T, W, VEC, MODE, PIPE, false>(p, st);
+  const int nb = p.K / W;
+  if (nb > 32) return launch_bfly_pc<T, W, VEC, MODE, PIPE, KV_COARSE>(p, st);
+  if constexpr (MODE == MODE_LDA && VEC && PIPE == 1) {
+    if (nb <= kSmallMaxBlocks) return launch_bfly_pc<T, W, VEC, MODE, PIPE, KV_SMALL>(p, st);
+  }
+  return launch_bfly_pc<T, W, VEC, MODE, PIPE, KV_FINE>(p, st);
 }
 
 template <typename T, int W, bool VEC, int MODE>
