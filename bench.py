@@ -334,9 +334,11 @@ def main():
         # a data loader does.  Every step moves its full inputs and result.
         h_theta = lda.theta.cpu().pin_memory()
         h_phi = lda.phi.cpu().pin_memory()
-        h_z = torch.empty(n_tok, dtype=torch.int32).pin_memory()
+        # z returns as int16 when K <= 32767 (exact; cast on the device, half the D2H bytes)
+        z_dt = torch.int16 if K <= 32767 else torch.int32
+        h_z = torch.empty(n_tok, dtype=z_dt).pin_memory()
         h2d = h_theta.numel() * h_theta.element_size() + h_phi.numel() * h_phi.element_size()
-        d2h = n_tok * 4
+        d2h = n_tok * h_z.element_size()
         lda.iterate_from_host(100, 2, h_theta, h_phi, h_z)  # warm-up (buffers, streams)
         torch.cuda.synchronize()
         barrier()
@@ -354,7 +356,8 @@ def main():
         e2e = {"value": total_tokens / float(et[0]), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(et[0]) * 1e3,
                "path": "DeviceLDA.iterate_from_host: pinned host theta/phi -> Gibbs iteration on the resident "
-                       "corpus -> z to host (next step's H2D and previous step's D2H overlap the current step)"}
+                       "corpus -> z (int16) to host (next step's H2D and previous step's D2H overlap the "
+                       "current step; bound by H2D, which shares L2 with the L2-bound draw)"}
         del h_theta, h_phi, h_z
         lda._host_pipe = None
 

@@ -162,7 +162,8 @@ class DeviceLDA:
         """n iterations, each ENTERED FROM HOST parameters: the drop-in
         gibbs_iterate(corpus, params, ...) call made with host theta/phi
         (pinned torch tensors) every iteration, z of each iteration returned
-        to z_host (pinned int32 [n_tokens]).  Every iteration moves its full
+        to z_host (pinned [n_tokens]; int32, or int16 when K <= 32767: the
+        topics are cast on the device, halving the D2H bytes).  Every iteration moves its full
         inputs and result across PCIe; the copies are pipelined the way a
         data loader prefetches: iteration s+1's H2D (copy stream) and
         iteration s-1's D2H (second copy stream) overlap iteration s, on two
@@ -175,6 +176,7 @@ class DeviceLDA:
                 "theta": [self.theta, block_aligned_rows(*self.theta.shape, self.theta.dtype, self.device, self.lanes)],
                 "phi": [self.phi, block_aligned_rows(*self.phi.shape, self.phi.dtype, self.device, self.lanes)],
                 "z": [self.z, torch.empty_like(self.z)],
+                "z16": [None, None],
                 "up": torch.cuda.Stream(), "down": torch.cuda.Stream(),
                 "ready": [torch.cuda.Event() for _ in range(2)],
                 "done": [torch.cuda.Event() for _ in range(2)],
@@ -205,9 +207,19 @@ class DeviceLDA:
             self.iterate(t0 + s)
             P["done"][i].record(st)
             if z_host is not None:
+                src = P["z"][i]
+                if z_host.dtype == torch.int16:
+                    if self.K > 32767:
+                        raise ValueError("int16 z needs K <= 32767")
+                    if P["z16"][i] is None:
+                        P["z16"][i] = torch.empty(self.z.numel(), dtype=torch.int16, device=self.device)
+                    st.wait_event(P["copied"][i])
+                    P["z16"][i].copy_(src)  # on the compute stream, behind the iteration
+                    P["done"][i].record(st)
+                    src = P["z16"][i]
                 down.wait_event(P["done"][i])
                 with torch.cuda.stream(down):
-                    z_host.copy_(P["z"][i], non_blocking=True)
+                    z_host.copy_(src, non_blocking=True)
                     P["copied"][i].record(down)
         st.wait_stream(down)
 

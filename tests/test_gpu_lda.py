@@ -175,3 +175,21 @@ def test_iterate_from_host_matches_resident_iterations():
     np.testing.assert_array_equal(h_z.numpy(), ref.z.cpu().numpy())
     np.testing.assert_array_equal(lda.theta.cpu().numpy(), ref.theta.cpu().numpy())
     np.testing.assert_array_equal(lda.phi.cpu().numpy(), ref.phi.cpu().numpy())
+
+
+def test_iterate_from_host_int16_z():
+    """int16 z transfer (K <= 32767) returns the same topics as int32."""
+    gen = np.random.default_rng(22)
+    M, V, K = 256, 500, 300
+    off, words = _corpus(gen, M, V, 25)
+    dc = wd.DeviceCorpus.from_csr(off, words)
+    lda = DeviceLDA(dc, K, V, seed=5)
+    lda.init_uniform()
+    h_theta = lda.theta.cpu().pin_memory()
+    h_phi = lda.phi.cpu().pin_memory()
+    z32 = torch.empty(dc.n_tokens, dtype=torch.int32).pin_memory()
+    z16 = torch.empty(dc.n_tokens, dtype=torch.int16).pin_memory()
+    lda.iterate_from_host(3, 2, h_theta, h_phi, z32)
+    lda.iterate_from_host(3, 2, h_theta, h_phi, z16)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(z16.numpy().astype(np.int32), z32.numpy())
