@@ -74,3 +74,22 @@ def test_two_ranks_reproduce_one(tmp_path):
         np.testing.assert_array_equal(p["wt"], one["wt"])
         np.testing.assert_array_equal(p["phi"], one["phi"])
         assert abs(float(p["ll"]) - float(one["ll"])) <= 1e-9 * abs(float(one["ll"]))
+
+
+def test_bench_nccl_path_world1():
+    """bench.py's N > 1 code path (NCCL process group, per-tile async count
+    all-reduces, max-over-ranks timing) exercised at world size 1 under
+    torchrun: one valid JSON line."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "1", "--force-dist", "--steps", "2",
+           "--warmup", "3", "--no-cpu", "--no-sampler", "--docs-per-gpu", "64000", "--vocab", "40000"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 1 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["config"]["vocab_tiles"] == 4
