@@ -65,8 +65,13 @@ class DeviceLDA:
         self._dt = _lib.WD_FLOAT32 if self.dtype == torch.float32 else _lib.WD_FLOAT64
         esz = 4 if self.dtype == torch.float32 else 8
         self.tiles = None
-        if vocab_tile_bytes and self.V * self.K * esz > vocab_tile_bytes:
-            rows = max(1, int(vocab_tile_bytes // (self.K * esz)))
+        if vocab_tile_bytes is not None:
+            # token order for the draw: vocabulary tiles (phi slices kept
+            # L2-resident) when phi exceeds vocab_tile_bytes, else one tile;
+            # either way (document, word)-ordered, so a document's repeated
+            # words reuse their phi row from L1 (kernels.VocabTiles)
+            tiled = vocab_tile_bytes > 0 and self.V * self.K * esz > vocab_tile_bytes
+            rows = max(1, int(vocab_tile_bytes // (self.K * esz))) if tiled else self.V
             if run_pad is None:
                 # pad (tile, document) runs to the lane-group height when runs
                 # are long enough that the padding (~L/2 slots per run) costs

@@ -205,8 +205,9 @@ class DeviceCorpus:
 class VocabTiles:
     """The corpus' tokens regrouped by vocabulary tile.
 
-    Tile t holds the tokens whose word lies in [t*rows, (t+1)*rows); inside a
-    tile the tokens keep CSR (document, position) order.  Drawing tile by tile
+    Tile t holds the tokens whose word lies in [t*rows, (t+1)*rows), ordered
+    by (document, word, position): documents stay contiguous and a
+    document's repeated words sit on adjacent rows (their phi loads hit L1).  Drawing tile by tile
     keeps the active slice of phi (rows x K) resident in the 126 MB L2 while
     theta rows stream; z, units and the hash keys still use each token's
     original (document, position), so results are bit-identical to the
@@ -236,7 +237,14 @@ class VocabTiles:
 def _build_vocab_tiles(corpus: "DeviceCorpus", rows_per_tile: int, run_pad: int = 0) -> VocabTiles:
     torch = _torch()
     tile = torch.div(corpus.words, rows_per_tile, rounding_mode="floor").to(torch.int32)
-    _, order = torch.sort(tile, stable=True)
+    # order: (tile, document, word).  Documents stay contiguous inside a tile
+    # (the draw's theta-segment sharing), and a document's repeated words
+    # become adjacent rows, whose phi loads then hit L1 instead of L2.
+    V = int(corpus.words.max().item()) + 1 if corpus.n_tokens else 1
+    M = max(1, corpus.n_docs)
+    key = (tile.to(torch.int64) * M + corpus.token_doc.to(torch.int64)) * V + corpus.words.to(torch.int64)
+    _, order = torch.sort(key, stable=True)
+    del key
     words = corpus.words[order].contiguous()
     doc = corpus.token_doc[order].contiguous()
     pos = (order - corpus.offsets[doc.long()]).to(torch.int32).contiguous()

@@ -149,7 +149,8 @@ def test_chi_square():
 def test_vocab_tile_builder_cpu(run_pad):
     """The vocabulary-tile regrouping (plain torch ops, runs on CPU tensors):
     every token appears exactly once with its (document, position); tiles
-    hold their word range in CSR order; with run_pad every (tile, document)
+    hold their word range ordered by (document, word, position); with
+    run_pad every (tile, document)
     run starts and ends on a multiple of run_pad, padding slots carry
     token_pos = -1 and their run's document."""
     import torch
@@ -177,7 +178,10 @@ def test_vocab_tile_builder_cpu(run_pad):
         a, b = t.bounds[ti], t.bounds[ti + 1]
         assert np.all(w[a:b] // rows == ti)
         rr = real[a:b]
-        assert np.all(np.diff(orig[np.cumsum(real)[a:b][rr] - 1]) > 0)  # CSR order inside the tile
+        o = orig[np.cumsum(real)[a:b][rr] - 1]  # original token index of the tile's real slots
+        dd, ww = d[a:b][rr].astype(np.int64), w[a:b][rr].astype(np.int64)
+        key = (dd * V + ww) * words.size + o
+        assert np.all(np.diff(key) > 0)  # (document, word, position) order
         if run_pad:
             assert (b - a) % run_pad == 0
             dd = d[a:b]
