@@ -446,8 +446,13 @@ def main():
                 "peak_source": peak_src,
                 "unit": "GB/s",
                 "frac": achieved / peak,
-                "traffic": (ncu.get("bfly_lda_k1024", {}).get("dram_bytes_per_draw") if K == 1024 else None),
-                "traffic_unit": "bytes per draw (ncu dram read+write, all vocabulary-tile launches)",
+                # per launch like `achieved` (which is the same ratio per draw):
+                # ncu dram read+write of the draw's vocabulary-tile launches / launches
+                "traffic": (ncu["bfly_lda_k1024"]["dram_bytes_per_draw"] / ncu["bfly_lda_k1024"]["launches_per_draw"]
+                            if K == 1024 and "bfly_lda_k1024" in ncu else None),
+                "traffic_unit": "bytes per launch (ncu dram read+write, mean over the vocabulary-tile launches)",
+                "algorithmic_bytes_per_launch": n_tok * bytes_per_tok / n_draw,
+                "launches_per_draw": n_draw,
                 "bytes_per_token": bytes_per_tok,
                 "draw_ms": draw_avg * 1e3,
                 "draw_share_of_step": draw_avg / per_step,
