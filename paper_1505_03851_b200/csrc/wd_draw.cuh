@@ -977,6 +977,94 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, K
   }
 }
 
+// ================================================ rows, one block
+// Standalone rows with K = NB * W (no remnant; dispatched for NB = 1): every block of a
+// chunk's 32 rows is staged in shared memory as it is loaded, so pass 2
+// reads the selected block from there instead of re-gathering it from
+// global memory (at K = 32 / 64 that per-lane re-gather -- 32 lines per
+// instruction -- made the per-row kernel L1-bound at ~2.7 / 4.8 TB/s).
+// Same loads, tree, running sums, bisection and walk as bfly_kernel.
+template <typename T, int W, int NB>
+__global__ void __launch_bounds__(128, 6) rows_stash_kernel(DrawParams<T> p) {
+  using GW = Geo<W>;
+  constexpr int E = GW::E, L = GW::L, R = GW::R;
+  constexpr int TS = W + 4;  // 16-byte aligned rows, conflict-free 128-bit accesses
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  T* tile = reinterpret_cast<T*>(smem_raw) + (size_t)wib * NB * 32 * TS;  // [NB][32 rows][TS]
+  const int s = lane % L;
+  const int rg = lane / L;
+  const int own = s * R + rg;  // interleaved rows (bfly_kernel, MODE_ROWS)
+  const int64_t n = p.n_tokens;
+  const int64_t n_chunks = (n + 31) >> 5;
+  const int64_t wpb = blockDim.x >> 5;
+  const uint64_t pol = make_l2_policy(p.l2_policy_x);
+  for (int64_t c = (int64_t)blockIdx.x * wpb + wib; c < n_chunks; c += (int64_t)gridDim.x * wpb) {
+    const int64_t tok0 = c << 5;
+    RowSet<T, L> prow;
+    RowSet<T, (L < 2 ? 2 : L)> trow;
+    prow.base = reinterpret_cast<const char*>(p.phi + s * E);
+    prow.ldb = (uint32_t)(p.ld_phi * sizeof(T));
+    trow.base = nullptr;
+    trow.ldb = 0;
+#pragma unroll
+    for (int i = 0; i < (L < 2 ? 2 : L); ++i) trow.idx[i] = 0;
+    bool rvalid[L];
+#pragma unroll
+    for (int kk = 0; kk < L; ++kk) {
+      const int k = kk * R + rg;
+      rvalid[kk] = tok0 + k < n;
+      prow.idx[kk] = (uint32_t)(rvalid[kk] ? tok0 + k : tok0);
+    }
+    T S[NB];
+    T acc = T(0);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      BlockRegs<T, W, true, MODE_ROWS, 1> cur;
+      cur.load(prow, trow, (int64_t)b * W, pol, pol);
+#pragma unroll
+      for (int kk = 0; kk < L; ++kk) store_seg(tile + ((size_t)b * 32 + kk * R + rg) * TS + s * E, cur.x[kk].v);
+      const T t = cur.reduce(rvalid, s, 0u);
+      acc = add_rn(acc, t);  // sequential running sums (kernels.py:221-223)
+      S[b] = acc;
+    }
+    __syncwarp();
+    const int64_t own_tok = tok0 + own;
+    if (own_tok < n) {
+      uint64_t ka, kb;
+      unsigned long long ekey;
+      int r;
+      int64_t zidx;
+      token_keys<T, MODE_ROWS>(p, own_tok, 0, W, ka, kb, ekey, r, zidx);
+      const T total = acc;
+      const T stop = make_stop<T>(p, zidx, total, ka, kb, true);
+      if (!(total > T(0))) atomicMin(p.err, ekey);
+      // bisection over the NB running sums: the first block whose sum exceeds stop
+      int j = NB - 1;
+#pragma unroll
+      for (int b = NB - 2; b >= 0; --b)
+        if (stop < S[b]) j = b;
+      const T prev = j > 0 ? S[j - 1] : T(0);
+      T high = S[j];
+      T cur[W];
+      const T* row = tile + ((size_t)j * 32 + own) * TS;
+#pragma unroll
+      for (int g = 0; g < W / E; ++g) {
+        T a[E];
+        load_seg_smem(a, row + g * E);
+#pragma unroll
+        for (int e = 0; e < E; ++e) cur[g * E + e] = a[e];
+      }
+      T low = prev;
+      int lo = 0;
+      Walk<T, W / 2>::run(cur, low, high, stop, r, lo);
+      p.z[zidx] = j * W + lo;
+    }
+    __syncwarp();
+  }
+}
+
 // ========================================================= prefix table
 // The paper's comparison baseline: a full per-token prefix-sum table
 // (kernels.py:129-167 compute_partial_sums_transposed + kernels.py:248-260
