@@ -11,7 +11,8 @@ from paper_1505_03851_b200.device_lda import DeviceLDA  # noqa: E402
 
 gen = np.random.default_rng(0)
 # standalone rows: scalar / vector / ring / coarse paths, fp32 + fp64, several W
-for K, W, dt in ((5, 32, np.float32), (19, 8, np.float64), (240, 32, np.float32), (1024, 32, np.float32),
+for K, W, dt in ((5, 32, np.float32), (32, 32, np.float32), (19, 8, np.float64), (240, 32, np.float32),
+                 (1024, 32, np.float32),
                  (4096, 32, np.float32), (130, 64, np.float32), (7, 2, np.float32)):
     w = torch.from_numpy(gen.uniform(0.1, 1, size=(70, K)).astype(dt)).cuda()
     wd.sample_rows(w, 1, lanes=W)
