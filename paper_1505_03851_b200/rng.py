@@ -73,3 +73,38 @@ def units_for(seed: int, *key_arrays, device_out: bool = False):
         return out.reshape(shape)
     res = out.cpu().numpy().reshape(shape)
     return res if shape else np.asarray(res)
+
+
+# ------------------------------------------------ opt-in Philox4x32-10 stream
+_PHILOX_M0, _PHILOX_M1 = 0xD2511F53, 0xCD9E8D57
+_PHILOX_W0, _PHILOX_W1 = 0x9E3779B9, 0xBB67AE85
+_M32 = np.uint64(0xFFFFFFFF)
+
+
+def philox4x32_10(ctr, key):
+    """Philox4x32 with 10 rounds (Salmon et al., SC'11; Random123's
+    philox4x32_R(10, ...)), vectorised over numpy arrays.  ctr: four uint32
+    arrays (or ints), key: two.  Host twin of philox_bits in
+    csrc/wd_device.cuh, pinned to the Random123 known-answer vectors in
+    tests/test_host_api.py."""
+    c = [np.asarray(x, dtype=np.uint64) & _M32 for x in ctr]
+    k0, k1 = (np.asarray(x, dtype=np.uint64) & _M32 for x in key)
+    for _ in range(10):
+        p0 = np.uint64(_PHILOX_M0) * c[0]
+        p1 = np.uint64(_PHILOX_M1) * c[2]
+        c = [(p1 >> np.uint64(32)) ^ c[1] ^ k0, p1 & _M32, (p0 >> np.uint64(32)) ^ c[3] ^ k1, p0 & _M32]
+        k0 = (k0 + np.uint64(_PHILOX_W0)) & _M32
+        k1 = (k1 + np.uint64(_PHILOX_W1)) & _M32
+    return c
+
+
+def philox_units(seed: int, a, b) -> np.ndarray:
+    """u in [0, 1) of PhiloxStops: counter (a lo, a hi, b lo, b hi) for global
+    document a and word position b, key = seed; 53 bits from the first two
+    output words (as the device does)."""
+    a = np.asarray(a, dtype=np.uint64)
+    b = np.asarray(b, dtype=np.uint64)
+    s = int(seed) & _MASK64
+    c = philox4x32_10([a & _M32, a >> np.uint64(32), b & _M32, b >> np.uint64(32)], [s & 0xFFFFFFFF, s >> 32])
+    bits = (c[0] << np.uint64(21)) | (c[1] >> np.uint64(11))
+    return bits.astype(np.float64) * _UNIT_SCALE

@@ -430,3 +430,23 @@ def test_lda_large_k_and_lanes_tiled_vs_oracle(K, W, dtype, run_pad):
     exp, err = O.draw_z_csr(theta, phi, off, words, W=W, seed=seed, threads=8)
     assert err is None
     np.testing.assert_array_equal(z, exp)
+
+
+@pytest.mark.parametrize("kernel", ["butterfly", "basic"])
+def test_philox_stops_match_host_twin(kernel):
+    """The opt-in Philox4x32-10 stream on the device (PhiloxStops) gives the
+    same z as the host twin's u injected per token (rng.philox_units, pinned
+    to the Random123 known answers)."""
+    gen = np.random.default_rng(31)
+    M, V, K = 96, 200, 200
+    N, off, words = _random_corpus(gen, M, V, 20)
+    theta = gen.uniform(0.05, 1, size=(M, K)).astype(np.float32)
+    phi = gen.uniform(0.05, 1, size=(V, K)).astype(np.float32)
+    dc = wd.DeviceCorpus.from_csr(off, words.astype(np.int32), doc_base=64)
+    seed = 0x1234_5678_9ABC
+    z_p = wd.draw_z_device(kernel, dc, _cuda(theta), _cuda(phi), wd.kernels.PhiloxStops(seed), 32).cpu().numpy()
+    doc = np.repeat(np.arange(M), N) + 64
+    pos = np.arange(int(off[-1])) - np.repeat(off[:-1], N)
+    u = wd.rng.philox_units(seed, doc, pos)
+    z_u = wd.draw_z_device(kernel, dc, _cuda(theta), _cuda(phi), _cuda(u), 32).cpu().numpy()
+    np.testing.assert_array_equal(z_p, z_u)

@@ -189,3 +189,19 @@ def test_vocab_tile_builder_cpu(run_pad):
             assert np.all(starts % run_pad == 0)
     if not run_pad:
         assert real.all()
+
+
+def test_philox_known_answers():
+    """Philox4x32-10 against the Random123 known-answer vectors (the opt-in
+    PhiloxStops stream; the device kernel is checked against this twin in
+    tests/test_gpu_parity.py)."""
+    from paper_1505_03851_b200.rng import philox4x32_10
+
+    kat = [
+        ([0, 0, 0, 0], [0, 0], [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]),
+        ([0xFFFFFFFF] * 4, [0xFFFFFFFF, 0xFFFFFFFF], [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]),
+        ([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0],
+         [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]),
+    ]
+    for ctr, key, out in kat:
+        assert [int(x) for x in philox4x32_10(ctr, key)] == out
