@@ -108,13 +108,20 @@ int launch_bfly_pc(const DrawParams<T>& p, cudaStream_t st) {
 // path with at most 16 blocks -> the cooperative pass-2 reload (measured:
 // K = 200 draw -3.5%; at K = 1024 it cost +6%, so larger K keep the per-lane
 // reload)
-constexpr int kSmallMaxBlocks = 16;
+#ifndef WD_SMALL_MAX_BLOCKS
+#define WD_SMALL_MAX_BLOCKS 16
+#endif
+constexpr int kSmallMaxBlocks = WD_SMALL_MAX_BLOCKS;
+constexpr int kSmallMinBlocks = 4;
 template <typename T, int W, bool VEC, int MODE, int PIPE>
 int launch_bfly_pipe(const DrawParams<T>& p, cudaStream_t st) {
   const int nb = p.K / W;
   if (nb > 32) return launch_bfly_pc<T, W, VEC, MODE, PIPE, KV_COARSE>(p, st);
   if constexpr (MODE == MODE_LDA && VEC && PIPE == 1) {
-    if (nb <= kSmallMaxBlocks) return launch_bfly_pc<T, W, VEC, MODE, PIPE, KV_SMALL>(p, st);
+    // measured: it pays on (document, word)-ordered tiles (DeviceLDA, K = 200:
+    // -3%) but not on a CSR-order draw (K = 16..240: +2..15%), nor below 4 blocks
+    if (nb >= kSmallMinBlocks && nb <= kSmallMaxBlocks && p.token_pos != nullptr)
+      return launch_bfly_pc<T, W, VEC, MODE, PIPE, KV_SMALL>(p, st);
   }
   return launch_bfly_pc<T, W, VEC, MODE, PIPE, KV_FINE>(p, st);
 }
