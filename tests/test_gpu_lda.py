@@ -193,3 +193,33 @@ def test_iterate_from_host_int16_z():
     lda.iterate_from_host(3, 2, h_theta, h_phi, z16)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(z16.numpy().astype(np.int32), z32.numpy())
+
+
+def test_theta_resample_wide_k_moments_and_long_document():
+    """K > 2048 takes the wide-K theta kernel (16-bit shared counters, output
+    row as scratch); a 70k-token document takes its global-count path.
+    Moments as in test_theta_resample_moments."""
+    K, alpha = 4096, 0.1
+    L = _lib.load()
+    gen = np.random.default_rng(3)
+    counts = np.zeros(K, dtype=np.int64)
+    counts[gen.choice(K, 40, replace=False)] = gen.integers(1, 9, size=40)
+    z_doc = np.repeat(np.arange(K), counts).astype(np.int32)
+    M = 3000
+    long_doc = np.repeat(np.arange(K), counts * 300).astype(np.int32)  # > 65535 tokens
+    z = np.concatenate([np.tile(z_doc, M), long_doc])
+    lens = [z_doc.size] * M + [long_doc.size]
+    off = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)).cuda()
+    theta = torch.empty((M + 1, K), dtype=torch.float32, device="cuda")
+    _lib.check(L.wd_resample_theta(0, torch.from_numpy(z).cuda().data_ptr(), off.data_ptr(), M + 1, K, alpha, 99, 0,
+                                   theta.data_ptr(), K, _lib.stream_handle()), "theta")
+    th = theta.cpu().numpy().astype(np.float64)
+    assert np.allclose(th.sum(1), 1.0, atol=1e-4)
+    a = alpha + counts
+    mean = a / a.sum()
+    se = np.sqrt(mean * (1 - mean) / (a.sum() + 1) / M)
+    hot = counts > 0
+    assert np.all(np.abs(th[:M, hot].mean(0) - mean[hot]) < 5 * se[hot] + 1e-7)
+    # the long document: Dir(alpha + 300 * counts) concentrates near its mean
+    a2 = alpha + 300 * counts
+    assert np.abs(th[M] - a2 / a2.sum()).max() < 0.02
