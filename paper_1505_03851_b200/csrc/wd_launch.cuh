@@ -67,13 +67,13 @@ inline int env_int(const char* name, int dflt) {
 }
 inline int pipe_variant(int mode, int nb) {
   // measured (profiles/): standalone rows -> one block in flight with the
-  // most warps (1) for <= 3 blocks per row, software pipelining (2) up to
-  // 15, the cp.async ring (5) from 16 (K = 4096: 5751 -> 6126 GB/s against
-  // pipelining); LDA -> one
+  // most warps (1) for <= 4 blocks per row, software pipelining (2) for 5-7,
+  // the cp.async ring (5) from 8 (K = 384 / 480 / 4096: 5894 / 5864 / 5751
+  // -> 6276 / 6374 / 6126 GB/s against pipelining); LDA -> one
   // block of register loads in flight (1): its gathers need the warps
   static int rows = env_int("WD_PIPE_ROWS", 0);
   static int lda = env_int("WD_PIPE_LDA", 1);
-  if (mode == MODE_ROWS) return rows ? rows : (nb <= 3 ? 1 : (nb >= 16 ? 5 : 2));
+  if (mode == MODE_ROWS) return rows ? rows : (nb <= 4 ? 1 : (nb <= 7 ? 2 : 5));
   return lda >= 5 ? 1 : lda;  // the ring does not pay for the LDA gathers (occupancy)
 }
 // L2 policies (0 normal, 1 evict_last, 2 evict_first); WD_L2_X / WD_L2_T override
