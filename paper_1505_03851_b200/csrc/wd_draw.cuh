@@ -8,8 +8,10 @@
 //   kernels.py:580-600  build_block_tables      -> bfly_kernel<..., ROWS>
 //   kernels.py:380-484  draw_z_basic/transposed -> prefix_kernel
 //
-// Layout and mapping:
-//   * one warp owns a CHUNK of 32 consecutive tokens (CSR order) or rows;
+// Layout and mapping (DESIGN.md sections 3-4):
+//   * one warp owns a CHUNK of 32 consecutive tokens (a vocabulary tile's
+//     (document, word) order, or CSR order) or rows; in LDA mode each lane
+//     group loads consecutive chunk rows, so its theta segments are shared;
 //   * the block loop walks W-topic blocks; per block every lane issues L
 //     vector loads, each covering E consecutive topics of one row, so a warp
 //     instruction reads R full contiguous row segments of W*sizeof(T) bytes
@@ -22,9 +24,13 @@
 //   * only the running block sums S_b are kept (shared memory, [b][lane]);
 //     the full K-entry table the reference stores (kernels.py:198-224) is
 //     never written: after the block bisection the selected block is
-//     re-read (L1/L2 hit) and its tree rebuilt in registers for the walk,
+//     re-read (per lane, or warp-cooperatively through a shared tile in the
+//     small-K variant) and its tree rebuilt in registers for the walk,
 //     which performs the same IEEE operations as the reference's
-//     cross-lane fetch walk.
+//     cross-lane fetch walk;
+//   * variants by K (KV): fine (<= 32 blocks per row), coarse (every G-th
+//     running sum), small (cooperative reload); rows_stash_kernel stages a
+//     single-block row (K = W) in shared memory during the load.
 #pragma once
 
 #include <cstdint>
