@@ -285,7 +285,10 @@ template <typename T, int W, bool VEC, int MODE, int ND> struct BlockRegs {
         }
         a[e] = MODE == MODE_LDA ? mul_rn(t, x[kk].v[e]) : x[kk].v[e];
       }
-      q[kk] = rvalid[kk] ? Tree<T, E>::sum(a) : T(0);
+      // rows of invalid tokens (padding, chunk tail) are summed too: they
+      // load valid rows, and a row's partials only ever reach its own
+      // (invalid, discarded) owner lane in the transpose-reduce
+      q[kk] = Tree<T, E>::sum(a);
     }
     return xreduce<T, L>(q, s);
   }
@@ -313,7 +316,7 @@ __device__ __forceinline__ T block_total_nd0(const RowSet<T, Geo<W>::L>& P,
       T a[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) a[e] = mul_rn(th[j].v[e], x[j].v[e]);
-      q[h + j] = rvalid[h + j] ? Tree<T, E>::sum(a) : T(0);
+      q[h + j] = Tree<T, E>::sum(a);  // invalid rows: see BlockRegs::reduce
     }
   }
   return xreduce<T, L>(q, s);
