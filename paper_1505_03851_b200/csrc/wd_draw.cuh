@@ -53,6 +53,10 @@ enum { MODE_LDA = 0, MODE_ROWS = 1 };
 #ifndef WD_MIN_BLOCKS_OTHER  // vector path, W != 32 or float64 rows
 #define WD_MIN_BLOCKS_OTHER 4
 #endif
+#ifndef WD_BLOCK_UNROLL  // unroll of the one-block-in-flight loop (address math amortised)
+#define WD_BLOCK_UNROLL 2  // measured: 1 -> 2 cfg4 draw -3.7%, cfg3 -3.9%; 4 is slower
+#endif
+constexpr int kBlockUnroll = WD_BLOCK_UNROLL;
 #ifndef WD_LDA_MIN_BLOCKS_COARSE  // K > 32 * W: the group recompute needs more registers
                                    // (measured at K = 4096: 4 -> 463 ms, 5 -> 415, 6 -> 468 per cfg5 draw)
 #define WD_LDA_MIN_BLOCKS_COARSE 5
@@ -352,6 +356,7 @@ __device__ __forceinline__ T bfly_blocks(const RowSet<T, Geo<W>::L>& prow,
       store_s(S, b, nb, G, lane, acc);
     }
   } else if (PIPE == 1 || PIPE == 4) {
+#pragma unroll (MODE == MODE_LDA ? kBlockUnroll : 1)  // rows: unrolling cost 3-5% at K = 64-128
     for (int b = 0; b < nb; ++b) {
       R cur;
       cur.load(prow, trow, (int64_t)b * W, px, pt);
