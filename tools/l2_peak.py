@@ -20,19 +20,26 @@ from torch.utils.cpp_extension import load_inline
 SRC = r"""
 #include <cuda_runtime.h>
 #include <torch/extension.h>
+// U independent 128-bit loads in flight per thread and iteration (the
+// single-load loop of the first version under-reported L2 bandwidth by ~25%)
+template <int U>
 __global__ void rd(const float4* __restrict__ p, long n, int reps, float* out) {
   float acc = 0.f;
+  const long stride = (long)gridDim.x * blockDim.x;
   for (int r = 0; r < reps; ++r)
-    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-      float4 v = __ldcg(p + i);
-      acc += v.x + v.y + v.z + v.w;
+    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i + (U - 1) * stride < n; i += U * stride) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldcg(p + i + u * stride);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
     }
   if (acc == 1234.5f) out[0] = acc;
 }
 void run(torch::Tensor x, int reps, torch::Tensor out, int blocks) {
   long n = x.numel() / 4;
-  rd<<<blocks, 512, 0, at::cuda::getCurrentCUDAStream()>>>((const float4*)x.data_ptr<float>(), n, reps,
-                                                          out.data_ptr<float>());
+  rd<8><<<blocks, 512, 0, at::cuda::getCurrentCUDAStream()>>>((const float4*)x.data_ptr<float>(), n, reps,
+                                                             out.data_ptr<float>());
 }
 """
 CPP = "void run(torch::Tensor x, int reps, torch::Tensor out, int blocks);"
@@ -50,10 +57,11 @@ def main():
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     out = torch.zeros(1, device="cuda")
     res = {}
-    for name, mb, reps in (("l2", a.mb, 200), ("hbm", 4096, 3)):
+    for name, mbs, reps in (("l2", [16, 24, 32, 40, 48], 200), ("hbm", [4096], 3)):
+      best, best_mb = 0.0, None
+      for mb in mbs:
         x = torch.rand(mb * (1 << 20) // 4, device="cuda")
-        best = 0.0
-        for blocks in (sms * 2, sms * 4, sms * 8):
+        for blocks in (sms * 2, sms * 4, sms * 8, sms * 16):
             mod.run(x, 1, out, blocks)
             torch.cuda.synchronize()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -61,11 +69,16 @@ def main():
             mod.run(x, reps, out, blocks)
             e.record()
             torch.cuda.synchronize()
-            gbs = x.numel() * 4 * reps / (s.elapsed_time(e) / 1e3) / 1e9
-            best = max(best, gbs)
-        res[f"{name}_read_gbs"] = best
-        res[f"{name}_buffer_mb"] = mb
+            # bytes actually read: whole U * stride sweeps only
+            stride = blocks * 512
+            n4 = x.numel() // 4
+            n_read = (n4 // (8 * stride)) * 8 * stride if n4 >= 8 * stride else 0
+            gbs = n_read * 16 * reps / (s.elapsed_time(e) / 1e3) / 1e9
+            if gbs > best:
+                best, best_mb = gbs, mb
         del x
+      res[f"{name}_read_gbs"] = best
+      res[f"{name}_buffer_mb"] = best_mb
     res["device"] = torch.cuda.get_device_name()
     print(json.dumps(res))
     if a.out:
