@@ -102,6 +102,7 @@ template <typename T, int E, bool VEC> struct Seg {
     for (int e = 0; e < E; ++e) v[e] = __ldg(p + e);
   }
   __device__ __forceinline__ void load(const T* __restrict__ p, uint64_t) { load(p); }
+  __device__ __forceinline__ void load_na(const T* __restrict__ p, uint64_t pol) { load(p, pol); }
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = T(0);
@@ -119,6 +120,12 @@ template <> struct Seg<float, 4, true> {
         : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
         : "l"(p), "l"(pol));
   }
+  // ... that does not allocate in L1 (rows streamed once per chunk)
+  __device__ __forceinline__ void load_na(const float* __restrict__ p, uint64_t pol) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+        : "l"(p), "l"(pol));
+  }
   __device__ __forceinline__ void zero() { v[0] = v[1] = v[2] = v[3] = 0.f; }
 };
 template <> struct Seg<float, 2, true> {
@@ -128,6 +135,7 @@ template <> struct Seg<float, 2, true> {
     v[0] = t.x; v[1] = t.y;
   }
   __device__ __forceinline__ void load(const float* __restrict__ p, uint64_t) { load(p); }
+  __device__ __forceinline__ void load_na(const float* __restrict__ p, uint64_t pol) { load(p, pol); }
   __device__ __forceinline__ void zero() { v[0] = v[1] = 0.f; }
 };
 template <> struct Seg<double, 4, true> {
@@ -138,6 +146,7 @@ template <> struct Seg<double, 4, true> {
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
   }
   __device__ __forceinline__ void load(const double* __restrict__ p, uint64_t) { load(p); }
+  __device__ __forceinline__ void load_na(const double* __restrict__ p, uint64_t pol) { load(p, pol); }
   __device__ __forceinline__ void zero() { v[0] = v[1] = v[2] = v[3] = 0.0; }
 };
 template <> struct Seg<double, 2, true> {
@@ -147,6 +156,7 @@ template <> struct Seg<double, 2, true> {
     v[0] = a.x; v[1] = a.y;
   }
   __device__ __forceinline__ void load(const double* __restrict__ p, uint64_t) { load(p); }
+  __device__ __forceinline__ void load_na(const double* __restrict__ p, uint64_t pol) { load(p, pol); }
   __device__ __forceinline__ void zero() { v[0] = v[1] = 0.0; }
 };
 

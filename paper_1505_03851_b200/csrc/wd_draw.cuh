@@ -57,6 +57,9 @@ enum { MODE_LDA = 0, MODE_ROWS = 1 };
 #define WD_BLOCK_UNROLL 2  // measured: 1 -> 2 cfg4 draw -3.7%, cfg3 -3.9%; 4 is slower
 #endif
 constexpr int kBlockUnroll = WD_BLOCK_UNROLL;
+#ifndef WD_PHI_L1NA  // LDA phi rows loaded with L1::no_allocate (each is read once per
+#define WD_PHI_L1NA 1  // chunk; keeps L1 for theta and the pass-2 reloads): cfg3 -1.8%, cfg4 -1.1%
+#endif
 #ifndef WD_LDA_MIN_BLOCKS_COARSE  // K > 32 * W: the group recompute needs more registers
                                    // (measured at K = 4096: 4 -> 463 ms, 5 -> 415, 6 -> 468 per cfg5 draw)
 #define WD_LDA_MIN_BLOCKS_COARSE 5
@@ -247,7 +250,10 @@ template <typename T, int W, bool VEC, int MODE, int ND> struct BlockRegs {
   __device__ __forceinline__ void load(const RowSet<T, L>& P, const RowSet<T, LT>& Q, int64_t off,
                                        uint64_t pol_x, uint64_t pol_t) {
 #pragma unroll
-    for (int kk = 0; kk < L; ++kk) x[kk].load(P.ptr(kk, off), pol_x);
+    for (int kk = 0; kk < L; ++kk) {
+      if (MODE == MODE_LDA && WD_PHI_L1NA) x[kk].load_na(P.ptr(kk, off), pol_x);
+      else x[kk].load(P.ptr(kk, off), pol_x);
+    }
     if (MODE == MODE_LDA) {
 #pragma unroll
       for (int i = 0; i < NT; ++i) th[i].load(Q.ptr(i, off), pol_t);
