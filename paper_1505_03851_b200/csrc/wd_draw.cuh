@@ -57,8 +57,8 @@ enum { MODE_LDA = 0, MODE_ROWS = 1 };
 #define WD_BLOCK_UNROLL 2  // measured: 1 -> 2 cfg4 draw -3.7%, cfg3 -3.9%; 4 is slower
 #endif
 constexpr int kBlockUnroll = WD_BLOCK_UNROLL;
-#ifndef WD_PHI_L1NA  // LDA phi rows loaded with L1::no_allocate (each is read once per
-#define WD_PHI_L1NA 1  // chunk; keeps L1 for theta and the pass-2 reloads): cfg3 -1.8%, cfg4 -1.1%
+#ifndef WD_PHI_L1NA  // LDA phi rows with L1::no_allocate (each read once per
+#define WD_PHI_L1NA 0  // chunk): uniform cfg3 -1.8%, cfg4 -1.1%, but Zipf cfg4 +30% (repeated words lose their L1 hits)
 #endif
 #ifndef WD_LDA_MIN_BLOCKS_COARSE  // K > 32 * W: the group recompute needs more registers
                                    // (measured at K = 4096: 4 -> 463 ms, 5 -> 415, 6 -> 468 per cfg5 draw)
