@@ -371,9 +371,11 @@ def test_vocab_tiled_draw_identical(kernel, run_pad):
     np.testing.assert_array_equal(z, exp)
 
 
-def test_full_size_lda_k1024_sampled_tokens():
+@pytest.mark.parametrize("words_kind", ["uniform", "zipf"])
+def test_full_size_lda_k1024_sampled_tokens(words_kind):
     """The bench shape (BASELINE configs[3] per GPU: 1M documents, Poisson(200)
-    lengths, V=40k, K=1024, vocabulary-tiled): 4096 randomly chosen tokens are
+    lengths, V=40k, K=1024, vocabulary-tiled, (document, word)-ordered and
+    run-padded), uniform and Zipf words: 4096 randomly chosen tokens are
     re-drawn one by one by the oracle from the same theta/phi rows, u and
     master-index key, and must match bit-for-bit; the fused word-topic counts
     must sum to the token count."""
@@ -385,11 +387,17 @@ def test_full_size_lda_k1024_sampled_tokens():
     off = torch.zeros(M + 1, dtype=torch.int64, device="cuda")
     off[1:] = torch.cumsum(lengths, 0)
     T = int(off[-1])
-    words = torch.randint(0, V, (T,), generator=g, device="cuda", dtype=torch.int32)
+    if words_kind == "uniform":
+        words = torch.randint(0, V, (T,), generator=g, device="cuda", dtype=torch.int32)
+    else:
+        p = 1.0 / torch.arange(1, V + 1, device="cuda", dtype=torch.float64)
+        cdf = torch.cumsum(p / p.sum(), 0)
+        words = torch.searchsorted(cdf, torch.rand(T, generator=g, device="cuda", dtype=torch.float64))
+        words = words.clamp_(max=V - 1).to(torch.int32)
     dc = wd.DeviceCorpus.from_csr(off, words)
     lda = DeviceLDA(dc, K, V, seed=11)
     lda.init_uniform()
-    assert lda.tiles is not None and lda.tiles.n_tiles == 4
+    assert lda.tiles is not None and lda.tiles.n_tiles == 4 and lda.tiles.run_pad == 8
     lda.draw(0)
     lda.check_errors()
     assert int(lda.word_topic.sum()) == T

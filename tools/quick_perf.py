@@ -3,7 +3,6 @@ import json
 import sys
 import time
 
-import numpy as np
 import torch
 
 sys.path.insert(0, ".")
