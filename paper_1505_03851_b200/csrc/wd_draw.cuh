@@ -197,6 +197,15 @@ __device__ __forceinline__ void load_first(T (&v)[E], const T* __restrict__ p, i
   for (int e = 0; e < E; ++e) v[e] = e < n ? __ldg(p + e) : T(0);
 }
 
+// 256-bit read-only global load (sm_100: LDG.E.256), 32-byte aligned address
+__device__ __forceinline__ void ld_v8(float (&a)[8], const float* p) {
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(a[0]), "=f"(a[1]), "=f"(a[2]), "=f"(a[3]), "=f"(a[4]), "=f"(a[5]), "=f"(a[6]), "=f"(a[7])
+      : "l"(p));
+}
+template <typename T>
+__device__ __forceinline__ void ld_v8(T (&)[8], const T*) {}  // (float only; never instantiated for T != float)
+
 // Levels log2(E)+1 .. log2(W) of the block trees: transpose-reduce of the L
 // per-lane partial sums q over lanes s ^ 1, s ^ 2, ... (the paper's butterfly
 // exchange).  Afterwards the lane holds the block total of row s*R + lane/L.
@@ -780,6 +789,35 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, K
         auto load_block = [&](int64_t base) {  // own row's products of one block
           constexpr int NG = W / E;
           constexpr int HG = NG >= 4 ? NG / 2 : NG;
+          if constexpr (sizeof(T) == 4 && VEC && E == 4 && W % 16 == 0) {
+            // 256-bit loads when the block is 32-byte aligned (block_aligned_rows
+            // layouts): each lane's 32 B are one whole sector, where a 128-bit
+            // load touches a sector per lane for half of its bytes
+            const T* xp = pown + base;
+            const T* tp = MODE == MODE_LDA ? town + base : xp;
+            if (((reinterpret_cast<uintptr_t>(xp) | reinterpret_cast<uintptr_t>(tp)) & 31) == 0) {
+              constexpr int N8 = W / 8;
+              constexpr int H8 = N8 >= 4 ? N8 / 2 : N8;
+#pragma unroll
+              for (int h = 0; h < N8; h += H8) {
+#pragma unroll
+                for (int g = h; g < h + H8; ++g) {
+                  float x8[8];
+                  ld_v8(x8, xp + g * 8);
+                  if (MODE == MODE_LDA) {
+                    float t8[8];
+                    ld_v8(t8, tp + g * 8);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) cur[g * 8 + e] = mul_rn(t8[e], x8[e]);
+                  } else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) cur[g * 8 + e] = x8[e];
+                  }
+                }
+              }
+              return;
+            }
+          }
 #pragma unroll
           for (int h = 0; h < NG; h += HG) {
 #pragma unroll
