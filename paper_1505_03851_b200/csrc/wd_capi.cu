@@ -13,11 +13,11 @@
 namespace wd {
 
 template <typename T>
-int launch_draw(int variant, int W, bool vec, int mode, const DrawParams<T>& p, void* ws,
+int launch_draw(int variant, int W, int vec, int mode, const DrawParams<T>& p, void* ws,
                 size_t ws_bytes, cudaStream_t st);
-extern template int launch_draw<float>(int, int, bool, int, const DrawParams<float>&, void*, size_t,
+extern template int launch_draw<float>(int, int, int, int, const DrawParams<float>&, void*, size_t,
                                        cudaStream_t);
-extern template int launch_draw<double>(int, int, bool, int, const DrawParams<double>&, void*, size_t,
+extern template int launch_draw<double>(int, int, int, int, const DrawParams<double>&, void*, size_t,
                                         cudaStream_t);
 
 static thread_local char g_last_err[256] = "";
@@ -120,8 +120,16 @@ static int draw_common(int variant, int lanes, int mode, DrawParams<T>& p, void*
       (mode == MODE_ROWS && (uint64_t)p.n_tokens >= (1ull << 32)))
     return WD_ERR_UNSUPPORTED;
   const int Weff = variant == WD_BUTTERFLY ? lanes : 32;
-  const bool vec = vec_ok(p.phi, p.ld_phi, p.K, Weff, sizeof(T)) &&
-                   (mode == MODE_ROWS || vec_ok(p.theta, p.ld_theta, p.K, Weff, sizeof(T)));
+  int vec = vec_ok(p.phi, p.ld_phi, p.K, Weff, sizeof(T)) &&
+            (mode == MODE_ROWS || vec_ok(p.theta, p.ld_theta, p.K, Weff, sizeof(T)));
+  // LDA, fp32, W = 32: 256-bit lane segments when every block start of phi and
+  // theta is 32-byte aligned (block_aligned_rows layouts)
+  auto a32 = [&](const void* ptr, int64_t ld) {
+    return ptr != nullptr && ((uintptr_t)ptr % 32) == 0 && (ld % 8) == 0 && ((p.K % Weff) % 8) == 0;
+  };
+  if (vec && variant == WD_BUTTERFLY && mode == MODE_LDA && sizeof(T) == 4 && lanes == 32 &&
+      a32(p.phi, p.ld_phi) && a32(p.theta, p.ld_theta))
+    vec = 2;
   return launch_draw<T>(variant, lanes, vec, mode, p, ws, ws_bytes, st);
 }
 

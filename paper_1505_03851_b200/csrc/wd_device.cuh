@@ -128,6 +128,25 @@ template <> struct Seg<float, 4, true> {
   }
   __device__ __forceinline__ void zero() { v[0] = v[1] = v[2] = v[3] = 0.f; }
 };
+// 256-bit segment (sm_100 LDG.E.256): 8 fp32 topics per lane, 32-byte aligned
+template <> struct Seg<float, 8, true> {
+  float v[8];
+  __device__ __forceinline__ void load(const float* __restrict__ p) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+        : "l"(p));
+  }
+  __device__ __forceinline__ void load(const float* __restrict__ p, uint64_t pol) {
+    asm("ld.global.nc.L2::cache_hint.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+        : "l"(p), "l"(pol));
+  }
+  __device__ __forceinline__ void load_na(const float* __restrict__ p, uint64_t pol) { load(p, pol); }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = 0.f;
+  }
+};
 template <> struct Seg<float, 2, true> {
   float v[2];
   __device__ __forceinline__ void load(const float* __restrict__ p) {
@@ -181,6 +200,13 @@ template <int W> struct Geo {
   static constexpr int L = W / E;
   static constexpr int R = 32 / L;
   static_assert(L >= 1 && L <= 32 && (L & (L - 1)) == 0, "W must be a power of two in [2, 128]");
+};
+// ... by vector level: V = 2 widens the lane segment to 8 fp32 topics (one
+// 256-bit load), so L halves: half the loads, shuffles and selects per block.
+template <int W, int V> struct GeoV {
+  static constexpr int E = (V == 2 && W >= 8) ? 8 : Geo<W>::E;
+  static constexpr int L = W / E;
+  static constexpr int R = 32 / L;
 };
 
 }  // namespace wd

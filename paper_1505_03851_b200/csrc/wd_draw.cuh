@@ -171,6 +171,10 @@ __device__ __forceinline__ void store_seg(double* p, const double (&a)[4]) {
   reinterpret_cast<double2*>(p)[0] = make_double2(a[0], a[1]);
   reinterpret_cast<double2*>(p)[1] = make_double2(a[2], a[3]);
 }
+__device__ __forceinline__ void store_seg(float* p, const float (&a)[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(a[0], a[1], a[2], a[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(a[4], a[5], a[6], a[7]);
+}
 template <typename T, int E>
 __device__ __forceinline__ void store_seg(T* p, const T (&a)[E]) {
 #pragma unroll
@@ -183,6 +187,11 @@ __device__ __forceinline__ void load_seg_smem(float (&a)[4], const float* p) {
 __device__ __forceinline__ void load_seg_smem(double (&a)[4], const double* p) {
   const double2 v0 = reinterpret_cast<const double2*>(p)[0], v1 = reinterpret_cast<const double2*>(p)[1];
   a[0] = v0.x; a[1] = v0.y; a[2] = v1.x; a[3] = v1.y;
+}
+__device__ __forceinline__ void load_seg_smem(float (&a)[8], const float* p) {
+  const float4 v0 = reinterpret_cast<const float4*>(p)[0], v1 = reinterpret_cast<const float4*>(p)[1];
+  a[0] = v0.x; a[1] = v0.y; a[2] = v0.z; a[3] = v0.w;
+  a[4] = v1.x; a[5] = v1.y; a[6] = v1.z; a[7] = v1.w;
 }
 template <typename T, int E>
 __device__ __forceinline__ void load_seg_smem(T (&a)[E], const T* p) {
@@ -248,12 +257,12 @@ template <typename T, int N> struct RowSet {
 // of phi (or weights) per lane, plus theta segments: ND = 1 when every row of
 // the chunk belongs to one document, ND = 2 when to two (rows pick theirs by
 // the bit mask dsel), ND = 0 one theta segment per row.
-template <typename T, int W, bool VEC, int MODE, int ND> struct BlockRegs {
-  static constexpr int E = Geo<W>::E, L = Geo<W>::L;
+template <typename T, int W, int VEC, int MODE, int ND> struct BlockRegs {
+  static constexpr int E = GeoV<W, VEC>::E, L = GeoV<W, VEC>::L;
   static constexpr int NT = MODE == MODE_LDA ? (ND == 0 ? L : ND) : 1;
   static constexpr int LT = L < 2 ? 2 : L;  // theta pointer slots (>= 2 for ND == 2)
-  Seg<T, E, VEC> x[L];
-  Seg<T, E, VEC> th[NT];
+  Seg<T, E, (VEC != 0)> x[L];
+  Seg<T, E, (VEC != 0)> th[NT];
   // every load is unconditional (invalid rows point at a valid row) so all
   // of them are in flight before the first use
   __device__ __forceinline__ void load(const RowSet<T, L>& P, const RowSet<T, LT>& Q, int64_t off,
@@ -315,16 +324,17 @@ template <typename T, int W, bool VEC, int MODE, int ND> struct BlockRegs {
 
 // Rows from more than two documents (LDA, ND = 0): theta is loaded per row,
 // in two half batches so at most L/2 (phi, theta) pairs are live at once.
-template <typename T, int W, bool VEC>
-__device__ __forceinline__ T block_total_nd0(const RowSet<T, Geo<W>::L>& P,
-                                             const RowSet<T, (Geo<W>::L < 2 ? 2 : Geo<W>::L)>& Q, int64_t off,
-                                             const bool (&rvalid)[Geo<W>::L], int s, uint64_t px, uint64_t pt) {
-  constexpr int E = Geo<W>::E, L = Geo<W>::L;
+template <typename T, int W, int VEC>
+__device__ __forceinline__ T block_total_nd0(const RowSet<T, GeoV<W, VEC>::L>& P,
+                                             const RowSet<T, (GeoV<W, VEC>::L < 2 ? 2 : GeoV<W, VEC>::L)>& Q,
+                                             int64_t off, const bool (&rvalid)[GeoV<W, VEC>::L], int s, uint64_t px,
+                                             uint64_t pt) {
+  constexpr int E = GeoV<W, VEC>::E, L = GeoV<W, VEC>::L;
   constexpr int H = L >= 4 ? L / 2 : L;
   T q[L];
 #pragma unroll
   for (int h = 0; h < L; h += H) {
-    Seg<T, E, VEC> x[H], th[H];
+    Seg<T, E, (VEC != 0)> x[H], th[H];
 #pragma unroll
     for (int j = 0; j < H; ++j) {
       x[j].load(P.ptr(h + j, off), px);
@@ -355,10 +365,10 @@ __device__ __forceinline__ void store_s(T* __restrict__ S, int b, int nb, int G,
 //   PIPE = 1  one block's loads in flight, then its arithmetic;
 //   PIPE = 2  block b+1's loads issued before block b's arithmetic;
 //   PIPE = 3  two blocks' loads issued together, then both reduced.
-template <typename T, int W, bool VEC, int MODE, int ND, int PIPE>
-__device__ __forceinline__ T bfly_blocks(const RowSet<T, Geo<W>::L>& prow,
-                                         const RowSet<T, (Geo<W>::L < 2 ? 2 : Geo<W>::L)>& trow,
-                                         const bool (&rvalid)[Geo<W>::L], int nb, int s, T acc,
+template <typename T, int W, int VEC, int MODE, int ND, int PIPE>
+__device__ __forceinline__ T bfly_blocks(const RowSet<T, GeoV<W, VEC>::L>& prow,
+                                         const RowSet<T, (GeoV<W, VEC>::L < 2 ? 2 : GeoV<W, VEC>::L)>& trow,
+                                         const bool (&rvalid)[GeoV<W, VEC>::L], int nb, int s, T acc,
                                          T* __restrict__ S, int lane, uint64_t px, uint64_t pt,
                                          uint32_t opaque_zero, uint32_t dsel, bool raw, int G) {
   // raw: store the block totals T_b themselves (the running sums are formed
@@ -510,7 +520,7 @@ __host__ __device__ constexpr int bfly_s_elems(int nbc, int rem, int TS, bool co
 // pass-2 reload it compiles (chosen per launch from nb = K / W).
 enum { KV_FINE = 0, KV_COARSE = 1, KV_SMALL = 2 };
 
-template <typename T, int W, bool VEC, int MODE, int PIPE, int KV>
+template <typename T, int W, int VEC, int MODE, int PIPE, int KV>
 constexpr int bfly_min_blocks() {
   constexpr bool COARSE = KV == KV_COARSE;
   if (sizeof(T) == 4 && W == 32 && VEC)
@@ -522,13 +532,13 @@ constexpr int bfly_min_blocks() {
   return 1;
 }
 
-template <typename T, int W, bool VEC, int MODE, int PIPE, int KV>
+template <typename T, int W, int VEC, int MODE, int PIPE, int KV>
 __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, KV>()))
     bfly_kernel(DrawParams<T> p) {
   // KV_COARSE: more than 32 blocks per row, every G-th running sum kept;
   // KV_SMALL (LDA, vector, at most 16 blocks): warp-cooperative pass-2 reload
   constexpr bool COARSE = KV == KV_COARSE;
-  using GW = Geo<W>;
+  using GW = GeoV<W, VEC>;
   constexpr int E = GW::E, L = GW::L, R = GW::R;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -652,11 +662,11 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, K
           if (s * E < rem) {
             const int k = row_of(kk);
             const bool full = s * E + E <= rem;  // else: partial segment, scalar loads
-            Seg<T, E, VEC> x;
+            Seg<T, E, (VEC != 0)> x;
             if (full) x.load(prow.ptr(kk, -rem)); else load_first(x.v, prow.ptr(kk, -rem), rem - s * E);
             T a[E];
             if (MODE == MODE_LDA) {
-              Seg<T, E, VEC> th;
+              Seg<T, E, (VEC != 0)> th;
               if (full) th.load(trow.ptr(kk, -rem)); else load_first(th.v, trow.ptr(kk, -rem), rem - s * E);
 #pragma unroll
               for (int e = 0; e < E; ++e) a[e] = mul_rn(th.v[e], x.v[e]);
@@ -751,7 +761,7 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, K
           T a[E];
           load_seg_smem(a, RT + own * TS + t);
           if (MODE == MODE_LDA) {  // the own document's theta remnant (L1-resident)
-            Seg<T, E, VEC> th;
+            Seg<T, E, (VEC != 0)> th;
             th.load(town + t);
 #pragma unroll
             for (int e = 0; e < E; ++e) a[e] = mul_rn(th.v[e], a[e]);
@@ -822,10 +832,10 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, K
           for (int h = 0; h < NG; h += HG) {
 #pragma unroll
             for (int g = h; g < h + HG; ++g) {
-              Seg<T, E, VEC> x;
+              Seg<T, E, (VEC != 0)> x;
               x.load(pown + base + g * E);
               if (MODE == MODE_LDA) {
-                Seg<T, E, VEC> th;
+                Seg<T, E, (VEC != 0)> th;
                 th.load(town + base + g * E);
 #pragma unroll
                 for (int e = 0; e < E; ++e) cur[g * E + e] = mul_rn(th.v[e], x.v[e]);
@@ -910,10 +920,10 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, K
         for (int h = 0; h < NG; h += HG) {
 #pragma unroll
           for (int g = h; g < h + HG; ++g) {
-            Seg<T, E, VEC> x;
+            Seg<T, E, (VEC != 0)> x;
             x.load(pown + base + g * E);
             if (MODE == MODE_LDA) {
-              Seg<T, E, VEC> th;
+              Seg<T, E, (VEC != 0)> th;
               th.load(town + base + g * E);
 #pragma unroll
               for (int e = 0; e < E; ++e) cur[g * E + e] = mul_rn(th.v[e], x.v[e]);
@@ -986,7 +996,7 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, K
           const int32_t dt = __shfl_sync(FULL, own_doc, t);
           const int bt = __shfl_sync(FULL, bbi, t);
           if ((wmask >> t) & 1u) {
-            Seg<T, E, VEC> x, th;
+            Seg<T, E, (VEC != 0)> x, th;
             x.load(p.phi + (int64_t)wt * p.ld_phi + bt + s * E);
             th.load(p.theta + (int64_t)dt * p.ld_theta + bt + s * E);
             T a[E];
@@ -1179,12 +1189,12 @@ __global__ void __launch_bounds__(128) prefix_kernel(DrawParams<T> p, T* __restr
         const int k = kk * R + rg;
         const int32_t wk = __shfl_sync(FULL, my_word, k);
         const int32_t dk = __shfl_sync(FULL, my_doc, k);
-        Seg<T, E, VEC> x;
+        Seg<T, E, (VEC != 0)> x;
         const bool v = tok0 + k < n;
         if (v) x.load(p.phi + (MODE == MODE_LDA ? (int64_t)wk : tok0 + k) * p.ld_phi + off + s * E);
         else x.zero();
         if (MODE == MODE_LDA) {
-          Seg<T, E, VEC> th;
+          Seg<T, E, (VEC != 0)> th;
           if (v) th.load(p.theta + (int64_t)dk * p.ld_theta + off + s * E); else th.zero();
 #pragma unroll
           for (int e = 0; e < E; ++e) x.v[e] = mul_rn(th.v[e], x.v[e]);

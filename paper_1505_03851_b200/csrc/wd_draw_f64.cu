@@ -2,5 +2,5 @@
 #include "wd_launch.cuh"
 
 namespace wd {
-template int launch_draw<double>(int, int, bool, int, const DrawParams<double>&, void*, size_t, cudaStream_t);
+template int launch_draw<double>(int, int, int, int, const DrawParams<double>&, void*, size_t, cudaStream_t);
 }  // namespace wd

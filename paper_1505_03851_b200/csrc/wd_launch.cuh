@@ -83,7 +83,7 @@ inline void l2_policies(int mode, int& px, int& pt) {
   pt = lt >= 0 ? lt : 0;
 }
 
-template <typename T, int W, bool VEC, int MODE, int PIPE, int KV>
+template <typename T, int W, int VEC, int MODE, int PIPE, int KV>
 int launch_bfly_pc(const DrawParams<T>& p, cudaStream_t st) {
   const void* fn = (const void*)bfly_kernel<T, W, VEC, MODE, PIPE, KV>;
   const size_t per_warp = bfly_smem_per_warp<T>(W, p.K, MODE, PIPE, VEC, KV);
@@ -114,7 +114,7 @@ int launch_bfly_pc(const DrawParams<T>& p, cudaStream_t st) {
 #endif
 constexpr int kSmallMaxBlocks = WD_SMALL_MAX_BLOCKS;
 constexpr int kSmallMinBlocks = 4;
-template <typename T, int W, bool VEC, int MODE, int PIPE>
+template <typename T, int W, int VEC, int MODE, int PIPE>
 int launch_bfly_pipe(const DrawParams<T>& p, cudaStream_t st) {
   const int nb = p.K / W;
   if (nb > 32) return launch_bfly_pc<T, W, VEC, MODE, PIPE, KV_COARSE>(p, st);
@@ -127,12 +127,12 @@ int launch_bfly_pipe(const DrawParams<T>& p, cudaStream_t st) {
   return launch_bfly_pc<T, W, VEC, MODE, PIPE, KV_FINE>(p, st);
 }
 
-template <typename T, int W, bool VEC, int MODE>
+template <typename T, int W, int VEC, int MODE>
 int launch_bfly_inst(const DrawParams<T>& p0, cudaStream_t st) {
   DrawParams<T> p = p0;
   l2_policies(MODE, p.l2_policy_x, p.l2_policy_t);
-  // the multi-block variants are instantiated for the fp32 W=32 vector path only
-  if constexpr (std::is_same<T, float>::value && W == 32 && VEC) {
+  // the multi-block variants are instantiated for the fp32 W=32 128-bit path only
+  if constexpr (std::is_same<T, float>::value && W == 32 && VEC == 1) {
     const int v = pipe_variant(MODE, p.K / W);
     if (v == 2) return launch_bfly_pipe<T, W, VEC, MODE, 2>(p, st);
     if (v == 3) return launch_bfly_pipe<T, W, VEC, MODE, 3>(p, st);
@@ -223,7 +223,7 @@ int launch_rows_stash(const DrawParams<T>& p0, cudaStream_t st) {
 // Dispatch on (variant, W, VEC, MODE); explicit instantiations live in
 // wd_draw_f32.cu / wd_draw_f64.cu so the two element types compile in parallel.
 template <typename T>
-int launch_draw(int variant, int W, bool vec, int mode, const DrawParams<T>& p, void* ws,
+int launch_draw(int variant, int W, int vec, int mode, const DrawParams<T>& p, void* ws,
                 size_t ws_bytes, cudaStream_t st) {
   if (variant == WD_BUTTERFLY) {
     // shared vector with a table workspace: build once, search per draw
@@ -231,8 +231,13 @@ int launch_draw(int variant, int W, bool vec, int mode, const DrawParams<T>& p, 
     if (mode == MODE_ROWS && p.ld_phi == 0 && ws != nullptr &&
         ws_bytes >= shared_table_elems(W, p.K) * sizeof(T))
       return launch_shared<T>(W, p, ws, st);
-    if (mode == MODE_LDA)
+    if (mode == MODE_LDA) {
+      if constexpr (std::is_same<T, float>::value) {
+        // 256-bit lane segments (vec 2: 32-byte aligned fp32 blocks, W = 32)
+        if (vec == 2 && W == 32) return launch_bfly_inst<T, 32, 2, MODE_LDA>(p, st);
+      }
       return vec ? launch_bfly_w<T, true, MODE_LDA>(W, p, st) : launch_bfly_w<T, false, MODE_LDA>(W, p, st);
+    }
     if constexpr (std::is_same<T, float>::value) {
       // K = W (fp32, W = 32): the single block staged in shared memory
       // (rows_stash_kernel; measured K = 32: 21.3 -> 27.4 G draws/s; staging

@@ -80,7 +80,11 @@ class DeviceLDA:
                 mean_run = corpus.n_tokens / max(1, corpus.n_docs) / n_tiles
                 # (fine instantiation only: at most 32 blocks per row)
                 fine = self.K // self.lanes <= 32
-                run_pad = self.lanes // 4 if (self.lanes >= 8 and fine and mean_run >= RUN_PAD_MIN_MEAN_RUN) else 0
+                # the kernel's lane-group height: 4 rows with 256-bit segments
+                # (fp32, W = 32, aligned rows), else W / 4 (measured at cfg4:
+                # padding to 4 vs 8 -1.2%, Zipf -2.2%)
+                group = 4 if (self.lanes == 32 and esz == 4) else self.lanes // 4
+                run_pad = group if (self.lanes >= 8 and fine and mean_run >= RUN_PAD_MIN_MEAN_RUN) else 0
             self.tiles = corpus.vocab_tiles(rows, run_pad)
         self._reducer = None  # in-flight per-tile count all-reduces (draw -> resample)
         n_err = self.tiles.n_tiles if self.tiles is not None else 1

@@ -397,7 +397,7 @@ def test_full_size_lda_k1024_sampled_tokens(words_kind):
     dc = wd.DeviceCorpus.from_csr(off, words)
     lda = DeviceLDA(dc, K, V, seed=11)
     lda.init_uniform()
-    assert lda.tiles is not None and lda.tiles.n_tiles == 4 and lda.tiles.run_pad == 8
+    assert lda.tiles is not None and lda.tiles.n_tiles == 4 and lda.tiles.run_pad == 4
     lda.draw(0)
     lda.check_errors()
     assert int(lda.word_topic.sum()) == T
