@@ -410,6 +410,10 @@ def main():
         cpu = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc}
 
     ncu = ncu_summary()
+    l2_bytes = None
+    if K == 1024 and "bfly_lda_k1024" in ncu:
+        l2_bytes = ncu["bfly_lda_k1024"].get("lts_tex_read_bytes_per_draw") or ncu["bfly_lda_k1024"].get(
+            "lts_bytes_per_draw")
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -458,12 +462,14 @@ def main():
                 "draw_share_of_step": draw_avg / per_step,
                 # the phi gathers are served from L2 by design (vocabulary
                 # tiles): the binding roofline is the measured L2 read peak
-                "l2": ({"achieved_gbs": (ncu["bfly_lda_k1024"]["lts_bytes_per_draw"] / draw_avg / 1e9),
+                "l2": ({"achieved_gbs": (l2_bytes / draw_avg / 1e9),
                         "peak_gbs": ncu.get("l2_read_peak_gbs"),
-                        "frac": (ncu["bfly_lda_k1024"]["lts_bytes_per_draw"] / draw_avg / 1e9)
-                        / ncu["l2_read_peak_gbs"],
-                        "note": "ncu lts__t_bytes per draw / CUDA-event draw time; peak from tools/l2_peak.py"}
-                       if K == 1024 and "bfly_lda_k1024" in ncu and ncu.get("l2_read_peak_gbs") else None),
+                        "frac": (l2_bytes / draw_avg / 1e9) / ncu["l2_read_peak_gbs"],
+                        "bytes_per_draw": l2_bytes,
+                        "note": "ncu L2 read bytes requested by the SMs per draw (lts__t_sectors_srcunit_tex_op_read"
+                                " x 32) / CUDA-event draw time; peak = streaming 256-bit L2 read kernel "
+                                "(tools/l2_peak.py)"}
+                       if l2_bytes and ncu.get("l2_read_peak_gbs") else None),
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
