@@ -127,8 +127,8 @@ static int draw_common(int variant, int lanes, int mode, DrawParams<T>& p, void*
   auto a32 = [&](const void* ptr, int64_t ld) {
     return ptr != nullptr && ((uintptr_t)ptr % 32) == 0 && (ld % 8) == 0 && ((p.K % Weff) % 8) == 0;
   };
-  if (vec && variant == WD_BUTTERFLY && mode == MODE_LDA && sizeof(T) == 4 && lanes == 32 &&
-      a32(p.phi, p.ld_phi) && a32(p.theta, p.ld_theta))
+  if (vec && variant == WD_BUTTERFLY && sizeof(T) == 4 && lanes == 32 && a32(p.phi, p.ld_phi) &&
+      (mode == MODE_ROWS || a32(p.theta, p.ld_theta)))
     vec = 2;
   return launch_draw<T>(variant, lanes, vec, mode, p, ws, ws_bytes, st);
 }

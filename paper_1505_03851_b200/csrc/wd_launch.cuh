@@ -15,6 +15,9 @@
 
 namespace wd {
 
+#ifndef WD_ROWS_V8
+#define WD_ROWS_V8 1
+#endif
 constexpr int kThreads = 128;          // 4 warps per CTA
 constexpr int kPrefixBlocksPerSM = 8;  // persistent grid of the prefix baseline
 
@@ -131,7 +134,11 @@ template <typename T, int W, int VEC, int MODE>
 int launch_bfly_inst(const DrawParams<T>& p0, cudaStream_t st) {
   DrawParams<T> p = p0;
   l2_policies(MODE, p.l2_policy_x, p.l2_policy_t);
-  // the multi-block variants are instantiated for the fp32 W=32 128-bit path only
+  // the multi-block variants are instantiated for the fp32 W=32 vector paths
+  // (the cp.async ring and the experimental 3/4 for 128-bit segments only)
+  if constexpr (std::is_same<T, float>::value && W == 32 && VEC == 2) {
+    if (pipe_variant(MODE, p.K / W) == 2) return launch_bfly_pipe<T, W, VEC, MODE, 2>(p, st);
+  }
   if constexpr (std::is_same<T, float>::value && W == 32 && VEC == 1) {
     const int v = pipe_variant(MODE, p.K / W);
     if (v == 2) return launch_bfly_pipe<T, W, VEC, MODE, 2>(p, st);
@@ -243,6 +250,9 @@ int launch_draw(int variant, int W, int vec, int mode, const DrawParams<T>& p, v
       // (rows_stash_kernel; measured K = 32: 21.3 -> 27.4 G draws/s; staging
       // two blocks at K = 64 was slower than the per-row kernel, 15.9 vs 18.5)
       if (vec && W == 32 && p.K == 32) return launch_rows_stash<T, 32, 1>(p, st);
+      // 256-bit segments while the block loop is register-resident (the
+      // cp.async ring from 8 blocks keeps 128-bit segments)
+      if (vec == 2 && W == 32 && p.K / 32 < 8 && WD_ROWS_V8) return launch_bfly_inst<T, 32, 2, MODE_ROWS>(p, st);
     }
     return vec ? launch_bfly_w<T, true, MODE_ROWS>(W, p, st) : launch_bfly_w<T, false, MODE_ROWS>(W, p, st);
   }
