@@ -106,8 +106,8 @@ static bool valid_lanes(int W) { return W == 2 || W == 4 || W == 8 || W == 16 ||
 static bool vec_ok(const void* ptr, int64_t ld, int K, int Weff, size_t esz) {
   if (ptr == nullptr) return true;
   const int E = Weff >= 4 ? 4 : Weff;
-  size_t vb = (size_t)E * esz;
-  if (vb > 16) vb = 16;
+  size_t vb = (size_t)E * esz;  // fp32: 16 B segments; fp64: 32 B (one 256-bit load)
+  if (vb > 32) vb = 32;
   const int64_t ve = (int64_t)(vb / esz);
   return ((uintptr_t)ptr % vb) == 0 && (ld % ve) == 0 && ((K % Weff) % ve) == 0;
 }

@@ -157,14 +157,17 @@ template <> struct Seg<float, 2, true> {
   __device__ __forceinline__ void load_na(const float* __restrict__ p, uint64_t pol) { load(p, pol); }
   __device__ __forceinline__ void zero() { v[0] = v[1] = 0.f; }
 };
+// 4 fp64 = one 256-bit load (the fp64 vector path requires 32-byte alignment)
 template <> struct Seg<double, 4, true> {
   double v[4];
   __device__ __forceinline__ void load(const double* __restrict__ p) {
-    double2 a = __ldg(reinterpret_cast<const double2*>(p));
-    double2 b = __ldg(reinterpret_cast<const double2*>(p + 2));
-    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
   }
-  __device__ __forceinline__ void load(const double* __restrict__ p, uint64_t) { load(p); }
+  __device__ __forceinline__ void load(const double* __restrict__ p, uint64_t pol) {
+    asm("ld.global.nc.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+        : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+        : "l"(p), "l"(pol));
+  }
   __device__ __forceinline__ void load_na(const double* __restrict__ p, uint64_t pol) { load(p, pol); }
   __device__ __forceinline__ void zero() { v[0] = v[1] = v[2] = v[3] = 0.0; }
 };
