@@ -199,10 +199,12 @@ def _random_corpus(gen, M, V, mean, zero_frac=0.05):
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("K", [1, 17, 64, 200, 1024, 8192])
+@pytest.mark.parametrize("K", [1, 17, 64, 100, 200, 1024, 8192])
 def test_lda_draw_vs_oracle(dtype, K):
     """Every kernel variant (all-remnant K < W, small, fine, coarse up to
-    K = 8192) against the oracle, fp32 and fp64."""
+    K = 8192; 256-bit segments when 32-byte aligned, 128-bit at K = 100
+    whose remnant of 4 breaks that alignment) against the oracle, fp32 and
+    fp64."""
     gen = np.random.default_rng(K)
     M, V = (1024, 700) if K <= 1024 else (128, 50)
     N, off, words = _random_corpus(gen, M, V, 30 if K < 1024 else 8)
