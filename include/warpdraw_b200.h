@@ -119,6 +119,11 @@ size_t wd_workspace_bytes(int variant, int dtype, int lanes, int32_t n_topics);
  *   z [n_tokens] int32 out.  word_topic [V x n_topics] / doc_topic
  *   [n_docs x n_topics] int32: optional (NULL = skip) fused count update
  *   (+= 1 per token, lda.py:174-182); the caller zeroes them.
+ *   Load width follows the alignment of the W-topic block starts (pointer,
+ *   leading dimension, n_topics mod lanes): 32-byte aligned fp32 blocks at
+ *   lanes = 32 use 256-bit segments, 16-byte aligned ones 128-bit segments
+ *   (fp64: 32-byte), others scalar loads -- identical results.
+ *   Token-list entries with token_pos < 0 are padding slots: loaded, never drawn.
  */
 int wd_draw_z(int variant, int dtype, int lanes, const void* theta, int64_t ld_theta,
               const void* phi, int64_t ld_phi, int32_t n_topics, const int64_t* doc_offsets,
