@@ -458,6 +458,9 @@ def main():
                 "algorithmic_bytes_per_launch": n_tok * bytes_per_tok / n_draw,
                 "launches_per_draw": n_draw,
                 "bytes_per_token": bytes_per_tok,
+                "note": "the phi gathers are served from L2 by design (vocabulary tiles keep each phi slice "
+                        "L2-resident), so algorithmic bytes / HBM peak exceeds 1; the binding roofline is "
+                        "roofline.l2 (SM L2 reads vs a streaming L2 read kernel); DRAM traffic = traffic",
                 "draw_ms": draw_avg * 1e3,
                 "draw_share_of_step": draw_avg / per_step,
                 # the phi gathers are served from L2 by design (vocabulary
