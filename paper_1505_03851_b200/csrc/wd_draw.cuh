@@ -60,6 +60,9 @@ constexpr int kBlockUnroll = WD_BLOCK_UNROLL;
 #ifndef WD_PHI_L1NA  // LDA phi rows with L1::no_allocate (each read once per
 #define WD_PHI_L1NA 0  // chunk): uniform cfg3 -1.8%, cfg4 -1.1%, but Zipf cfg4 +30% (repeated words lose their L1 hits)
 #endif
+#ifndef WD_LDA_MIN_BLOCKS_SMALL  // small-K variant with 256-bit segments
+#define WD_LDA_MIN_BLOCKS_SMALL 7  // measured cfg3: 6 -> 16.3 ms, 7 -> 15.6, 8 -> 19.6 (spills)
+#endif
 #ifndef WD_LDA_MIN_BLOCKS_COARSE  // K > 32 * W: the group recompute needs more registers
                                    // (measured at K = 4096: 4 -> 463 ms, 5 -> 415, 6 -> 468 per cfg5 draw)
 #define WD_LDA_MIN_BLOCKS_COARSE 5
@@ -524,7 +527,11 @@ template <typename T, int W, int VEC, int MODE, int PIPE, int KV>
 constexpr int bfly_min_blocks() {
   constexpr bool COARSE = KV == KV_COARSE;
   if (sizeof(T) == 4 && W == 32 && VEC)
-    return PIPE == 2 ? 4 : (MODE == MODE_LDA ? (COARSE ? WD_LDA_MIN_BLOCKS_COARSE : WD_LDA_MIN_BLOCKS) : 8);
+    return PIPE == 2 ? 4
+                     : (MODE == MODE_LDA ? (COARSE ? WD_LDA_MIN_BLOCKS_COARSE
+                                                   : (KV == KV_SMALL && VEC == 2 ? WD_LDA_MIN_BLOCKS_SMALL
+                                                                                 : WD_LDA_MIN_BLOCKS))
+                                         : 8);
   if (sizeof(T) == 8 && W == 32 && VEC && MODE == MODE_LDA) return WD_LDA_MIN_BLOCKS_F64;
   // other lane counts: uncapped they take 150-250 registers (float64 W = 64
   // would spill at 4 CTAs)
