@@ -27,11 +27,17 @@ void set_last_cuda_error(cudaError_t e);
 inline int occupancy_blocks(const void* fn, size_t smem, int threads = kThreads) {
   static std::mutex mu;
   static std::map<std::pair<const void*, size_t>, int> cache;
+  static std::map<const void*, size_t> smem_attr;  // per kernel: the largest opt-in set so far
   std::lock_guard<std::mutex> lock(mu);
+  // the opt-in dynamic shared memory limit is per function: only ever raise it
+  // (a smaller request after a larger one must not lower it under a cached launch)
+  if (smem > 48 * 1024 && smem > smem_attr[fn]) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_attr[fn] = smem;
+  }
   auto key = std::make_pair(fn, smem * 1024 + (size_t)threads);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int nb = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem);
   if (e != cudaSuccess) {

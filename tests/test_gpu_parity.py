@@ -83,6 +83,17 @@ def test_rows_vs_oracle(dtype, K):
     np.testing.assert_array_equal(got, exp)
 
 
+def test_rows_kernel_smem_revisit():
+    """One kernel instantiation launched with a large, then a smaller, then the
+    large dynamic shared-memory size again (the opt-in limit is per function and
+    must never be lowered under a cached launch configuration)."""
+    gen = np.random.default_rng(5)
+    for K in (1024, 512, 1024, 2048, 512, 2048):
+        w = gen.uniform(0.1, 1.0, size=(1024, K)).astype(np.float32)
+        got = wd.sample_rows(_cuda(w), K, lanes=32).cpu().numpy()
+        np.testing.assert_array_equal(got, O.sample_rows(w, 32, wd.derive_seed(K, 6), threads=8), err_msg=f"K={K}")
+
+
 @pytest.mark.parametrize("W", [2, 4, 16, 64])
 def test_rows_other_lane_counts_vs_oracle(W):
     gen = np.random.default_rng(W)
