@@ -40,6 +40,30 @@ def test_theta_resample_moments():
     assert np.all(np.abs(th.mean(0) - mean) < 5 * se + 1e-7), (th.mean(0), mean)
 
 
+@pytest.mark.parametrize("alpha", [0.1, 0.35, 0.5, 1.5])
+def test_theta_resample_marginals_are_beta(alpha):
+    """Dirichlet marginals: theta_k ~ Beta(a_k, sum(a) - a_k).  Kolmogorov-Smirnov
+    over 20k documents sharing one count vector, for zero-count topics (shape
+    alpha < 1: the boosted Marsaglia-Tsang path, and alpha = 1.5) and non-zero
+    ones; threshold p > 1e-4 per topic."""
+    stats = pytest.importorskip("scipy.stats")
+    K, M = 64, 20000
+    L = _lib.load()
+    counts = np.zeros(K, dtype=np.int64)
+    counts[[1, 5, 9, 40, 63]] = [1, 2, 7, 30, 3]
+    z_doc = np.repeat(np.arange(K), counts).astype(np.int32)
+    z = torch.from_numpy(np.tile(z_doc, M)).cuda()
+    off = torch.arange(0, (M + 1) * z_doc.size, z_doc.size, dtype=torch.int64, device="cuda")
+    theta = torch.empty((M, K), dtype=torch.float32, device="cuda")
+    _lib.check(L.wd_resample_theta(0, z.data_ptr(), off.data_ptr(), M, K, alpha, 777, 0, theta.data_ptr(), K,
+                                   _lib.stream_handle()), "theta")
+    th = theta.cpu().numpy().astype(np.float64)
+    a = alpha + counts
+    for k in (0, 1, 2, 5, 9, 40, 63):
+        p = stats.kstest(th[:, k], stats.beta(a[k], a.sum() - a[k]).cdf).pvalue
+        assert p > 1e-4, (k, p)
+
+
 def test_phi_resample_columns_normalised_and_deterministic():
     V, K, beta = 3000, 64, 0.01
     gen = np.random.default_rng(0)
