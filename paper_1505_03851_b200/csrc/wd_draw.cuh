@@ -563,6 +563,10 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, K
   // warp-cooperative pass-2 reload (LDA, vector, fine): with no remnant tile
   // the reload tile aliases S, which is then sized for it
   constexpr bool COOP = MODE == MODE_LDA && VEC && KV == KV_SMALL;
+  // rows with pipelined block loads: the remnant prefix is stored for a
+  // vector fallback scan (measured: K = 176-240 +5%; the PIPE 1 variant, K <= 144,
+  // lost 13% at K = 16 and keeps the re-adding scan)
+  constexpr bool kPrefixScan = MODE == MODE_ROWS && PIPE >= 2;
   const size_t SW = (size_t)bfly_s_elems(nbc, rem, TS, COOP);  // S elements per warp
   T* S = reinterpret_cast<T*>(smem_raw) + (size_t)wib * SW;
   T* RT = reinterpret_cast<T*>(smem_raw) + (size_t)wpb_i * SW + (size_t)wib * 32 * TS;
@@ -774,7 +778,15 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, K
             for (int e = 0; e < E; ++e) a[e] = mul_rn(th.v[e], a[e]);
           }
 #pragma unroll
-          for (int e = 0; e < E; ++e) prem = add_rn(prem, a[e]);
+          for (int e = 0; e < E; ++e) {
+            prem = add_rn(prem, a[e]);
+            a[e] = prem;
+          }
+          // rows: the own row's remnant prefix P[t] replaces its products, so
+          // the remnant fallback scans it without re-adding (a chain of
+          // dependent shared loads and adds before; LDA keeps the products:
+          // its tuned register allocation spills with the store)
+          if constexpr (kPrefixScan) store_seg(RT + own * TS + t, a);
         }
       }
       acc = prem;
@@ -896,7 +908,20 @@ __global__ void __launch_bounds__(128, (bfly_min_blocks<T, W, VEC, MODE, PIPE, K
           Walk<T, W / 2>::run(cur, low, high, stop, r, lo);
           result = (int)bb + lo;
         }
-        if (fallback) {
+        if (kPrefixScan && fallback && async_rem) {
+          // linear remnant fallback (kernels.py:354-361) over the prefix P[t]
+          // the raw pass stored (the same sequential sums): first t with
+          // stop < P[t], one vector shared load per E topics
+          int found = -1;
+          for (int t = 0; t < rem && found < 0; t += E) {
+            T pv[E];
+            load_seg_smem(pv, RT + own * TS + t);
+#pragma unroll
+            for (int e = E - 1; e >= 0; --e)
+              if (stop < pv[e]) found = t + e;
+          }
+          if (found >= 0) result = found;
+        } else if (fallback) {
           // linear remnant fallback (kernels.py:354-361), products from the tile(s)
           T a2 = T(0);
           for (int t = 0; t < rem; ++t) {
