@@ -1165,6 +1165,99 @@ __global__ void __launch_bounds__(128, 6) rows_stash_kernel(DrawParams<T> p) {
   }
 }
 
+// rows_stash_kernel with the chunk loads double-buffered by cp.async
+// (fp32, 16-byte segments): chunk c + stride is in flight while chunk c is
+// reduced and searched, so each warp always has one chunk of loads
+// outstanding (the single-buffer kernel exposed a DRAM round trip per chunk:
+// K = 32 at 49% of DRAM bandwidth with 22 warps per SM).  Same arithmetic,
+// same results.
+template <typename T, int W, int NB>
+__global__ void __launch_bounds__(128, (NB == 1 ? 6 : 3)) rows_stash2_kernel(DrawParams<T> p) {
+  using GW = Geo<W>;
+  constexpr int E = GW::E, L = GW::L, R = GW::R;
+  static_assert(E * sizeof(T) == 16, "16-byte segments");
+  constexpr int TS = W + 4;
+  constexpr int STAGE = NB * 32 * TS;  // elements per stage
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  T* tiles = reinterpret_cast<T*>(smem_raw) + (size_t)wib * 2 * STAGE;  // [2][NB][32 rows][TS]
+  const int s = lane % L;
+  const int rg = lane / L;
+  const int own = s * R + rg;
+  const int64_t n = p.n_tokens;
+  const int64_t n_chunks = (n + 31) >> 5;
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  auto issue = [&](int64_t c, T* tile) {
+    const int64_t tok0 = c << 5;
+#pragma unroll
+    for (int kk = 0; kk < L; ++kk) {
+      const int k = kk * R + rg;
+      const int64_t row = tok0 + k < n ? tok0 + k : tok0;  // tail rows read a valid row
+      const T* src = p.phi + row * p.ld_phi + s * E;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) cp_async16(tile + ((size_t)b * 32 + k) * TS + s * E, src + b * W);
+    }
+    cp_async_commit();
+  };
+  int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (c < n_chunks) issue(c, tiles);
+  for (int st = 0; c < n_chunks; c += stride, st ^= 1) {
+    if (c + stride < n_chunks) issue(c + stride, tiles + (st ^ 1) * STAGE);
+    else cp_async_commit();  // empty group: the wait below still means "chunk c landed"
+    cp_async_wait_n<1>();
+    __syncwarp();
+    T* tile = tiles + st * STAGE;
+    const int64_t tok0 = c << 5;
+    bool rvalid[L];
+#pragma unroll
+    for (int kk = 0; kk < L; ++kk) rvalid[kk] = tok0 + kk * R + rg < n;
+    T S[NB];
+    T acc = T(0);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      BlockRegs<T, W, true, MODE_ROWS, 1> cur;
+#pragma unroll
+      for (int kk = 0; kk < L; ++kk) load_seg_smem(cur.x[kk].v, tile + ((size_t)b * 32 + kk * R + rg) * TS + s * E);
+      const T t = cur.reduce(rvalid, s, 0u);
+      acc = add_rn(acc, t);  // sequential running sums (kernels.py:221-223)
+      S[b] = acc;
+    }
+    const int64_t own_tok = tok0 + own;
+    if (own_tok < n) {
+      uint64_t ka, kb;
+      unsigned long long ekey;
+      int r;
+      int64_t zidx;
+      token_keys<T, MODE_ROWS>(p, own_tok, 0, W, ka, kb, ekey, r, zidx);
+      const T total = acc;
+      const T stop = make_stop<T>(p, zidx, total, ka, kb, true);
+      if (!(total > T(0))) atomicMin(p.err, ekey);
+      int j = NB - 1;
+#pragma unroll
+      for (int b = NB - 2; b >= 0; --b)
+        if (stop < S[b]) j = b;
+      const T prev = j > 0 ? S[j - 1] : T(0);
+      T high = S[j];
+      T cur[W];
+      const T* row = tile + ((size_t)j * 32 + own) * TS;
+#pragma unroll
+      for (int g = 0; g < W / E; ++g) {
+        T a[E];
+        load_seg_smem(a, row + g * E);
+#pragma unroll
+        for (int e = 0; e < E; ++e) cur[g * E + e] = a[e];
+      }
+      T low = prev;
+      int lo = 0;
+      Walk<T, W / 2>::run(cur, low, high, stop, r, lo);
+      p.z[zidx] = j * W + lo;
+    }
+    __syncwarp();  // every lane is done with this stage before it is refilled
+  }
+  cp_async_wait_n<0>();
+}
+
 // ========================================================= prefix table
 // The paper's comparison baseline: a full per-token prefix-sum table
 // (kernels.py:129-167 compute_partial_sums_transposed + kernels.py:248-260

@@ -15,6 +15,10 @@
 
 namespace wd {
 
+// bit 0: K = 32 through the double-buffered stash kernel; bit 1: K = 64 too
+#ifndef WD_STASH2
+#define WD_STASH2 1
+#endif
 #ifndef WD_ROWS_V8
 #define WD_ROWS_V8 1
 #endif
@@ -211,15 +215,15 @@ int launch_shared(int W, const DrawParams<T>& p, void* ws, cudaStream_t st) {
   }
 }
 
-template <typename T, int W, int NB>
+template <typename T, int W, int NB, int NS = 1>
 int launch_rows_stash(const DrawParams<T>& p0, cudaStream_t st) {
   DrawParams<T> p = p0;
   int px = 0, pt = 0;
   l2_policies(MODE_ROWS, px, pt);
   p.l2_policy_x = px;
-  const void* fn = (const void*)rows_stash_kernel<T, W, NB>;
+  const void* fn = NS == 2 ? (const void*)rows_stash2_kernel<T, W, NB> : (const void*)rows_stash_kernel<T, W, NB>;
   const int wpb = kThreads / 32;
-  const size_t smem = (size_t)wpb * NB * 32 * (W + 4) * sizeof(T);
+  const size_t smem = (size_t)NS * wpb * NB * 32 * (W + 4) * sizeof(T);
   const int per_sm = occupancy_blocks(fn, smem, kThreads);
   if (per_sm <= 0) return WD_ERR_CUDA;
   const int64_t chunks = (p.n_tokens + 31) / 32;
@@ -227,7 +231,8 @@ int launch_rows_stash(const DrawParams<T>& p0, cudaStream_t st) {
   const int64_t cap = (int64_t)per_sm * device_sm_count();
   const int grid = (int)(want < cap ? want : cap);
   if (grid <= 0) return WD_OK;
-  rows_stash_kernel<T, W, NB><<<grid, kThreads, smem, st>>>(p);
+  if constexpr (NS == 2) rows_stash2_kernel<T, W, NB><<<grid, kThreads, smem, st>>>(p);
+  else rows_stash_kernel<T, W, NB><<<grid, kThreads, smem, st>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { set_last_cuda_error(e); return WD_ERR_CUDA; }
   return WD_OK;
@@ -255,7 +260,15 @@ int launch_draw(int variant, int W, int vec, int mode, const DrawParams<T>& p, v
       // K = W (fp32, W = 32): the single block staged in shared memory
       // (rows_stash_kernel; measured K = 32: 21.3 -> 27.4 G draws/s; staging
       // two blocks at K = 64 was slower than the per-row kernel, 15.9 vs 18.5)
-      if (vec && W == 32 && p.K == 32) return launch_rows_stash<T, 32, 1>(p, st);
+      // K = 32: the double-buffered variant (rows_stash2_kernel, measured
+      // 26.5 -> 27.9 G draws/s; at K = 64, two blocks per stage, 20.4 -> 18.6)
+      if (vec && W == 32 && p.K == 32) {
+        if (WD_STASH2 & 1) return launch_rows_stash<T, 32, 1, 2>(p, st);
+        return launch_rows_stash<T, 32, 1>(p, st);
+      }
+#if WD_STASH2 & 2
+      if (vec && W == 32 && p.K == 64) return launch_rows_stash<T, 32, 2, 2>(p, st);
+#endif
       // 256-bit segments while the block loop is register-resident (the
       // cp.async ring from 8 blocks keeps 128-bit segments)
       if (vec == 2 && W == 32 && p.K / 32 < 8 && WD_ROWS_V8) return launch_bfly_inst<T, 32, 2, MODE_ROWS>(p, st);
