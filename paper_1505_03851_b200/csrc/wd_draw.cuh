@@ -1167,10 +1167,14 @@ __global__ void __launch_bounds__(128, 6) rows_stash_kernel(DrawParams<T> p) {
 
 // rows_stash_kernel with the chunk loads double-buffered by cp.async
 // (fp32, 16-byte segments): chunk c + stride is in flight while chunk c is
-// reduced and searched, so each warp always has one chunk of loads
-// outstanding (the single-buffer kernel exposed a DRAM round trip per chunk:
-// K = 32 at 49% of DRAM bandwidth with 22 warps per SM).  Same arithmetic,
-// same results.
+// searched, so each warp always has one chunk of loads outstanding (the
+// single-buffer kernel exposed a DRAM round trip per chunk: K = 32 at 49% of
+// DRAM bandwidth with 22 warps per SM).  The loads are coalesced (a warp
+// instruction copies R whole row segments); each lane then reads ITS OWN row
+// from the tile and forms the block totals as the pairwise tree in registers
+// -- the same additions the shuffle transpose-reduce performs, so the same
+// bits, without its shuffles and second pass over the tile (ncu: the
+// transposed variant was short-scoreboard / shared-memory bound).
 template <typename T, int W, int NB>
 __global__ void __launch_bounds__(128, (NB == 1 ? 6 : 3)) rows_stash2_kernel(DrawParams<T> p) {
   using GW = Geo<W>;
@@ -1184,7 +1188,7 @@ __global__ void __launch_bounds__(128, (NB == 1 ? 6 : 3)) rows_stash2_kernel(Dra
   T* tiles = reinterpret_cast<T*>(smem_raw) + (size_t)wib * 2 * STAGE;  // [2][NB][32 rows][TS]
   const int s = lane % L;
   const int rg = lane / L;
-  const int own = s * R + rg;
+  const int own = lane;  // own row: consecutive lanes read rows TS apart (conflict-free)
   const int64_t n = p.n_tokens;
   const int64_t n_chunks = (n + 31) >> 5;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -1209,49 +1213,50 @@ __global__ void __launch_bounds__(128, (NB == 1 ? 6 : 3)) rows_stash2_kernel(Dra
     __syncwarp();
     T* tile = tiles + st * STAGE;
     const int64_t tok0 = c << 5;
-    bool rvalid[L];
+    {
+      // the lane reads its own row from the tile and forms each block total
+      // as the same pairwise tree the transpose-reduce computes (no
+      // shuffles); pass 2 re-reads the selected block from the tile
+      const int64_t own_tok = tok0 + own;
+      if (own_tok < n) {
+        const T* row = tile + (size_t)own * TS;
+        T cur[W];
+        auto load_own = [&](int b) {
 #pragma unroll
-    for (int kk = 0; kk < L; ++kk) rvalid[kk] = tok0 + kk * R + rg < n;
-    T S[NB];
-    T acc = T(0);
+          for (int g = 0; g < W / E; ++g) {
+            T a[E];
+            load_seg_smem(a, row + (size_t)b * 32 * TS + g * E);
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      BlockRegs<T, W, true, MODE_ROWS, 1> cur;
+            for (int e = 0; e < E; ++e) cur[g * E + e] = a[e];
+          }
+        };
+        T S[NB];
+        T acc = T(0);
 #pragma unroll
-      for (int kk = 0; kk < L; ++kk) load_seg_smem(cur.x[kk].v, tile + ((size_t)b * 32 + kk * R + rg) * TS + s * E);
-      const T t = cur.reduce(rvalid, s, 0u);
-      acc = add_rn(acc, t);  // sequential running sums (kernels.py:221-223)
-      S[b] = acc;
-    }
-    const int64_t own_tok = tok0 + own;
-    if (own_tok < n) {
-      uint64_t ka, kb;
-      unsigned long long ekey;
-      int r;
-      int64_t zidx;
-      token_keys<T, MODE_ROWS>(p, own_tok, 0, W, ka, kb, ekey, r, zidx);
-      const T total = acc;
-      const T stop = make_stop<T>(p, zidx, total, ka, kb, true);
-      if (!(total > T(0))) atomicMin(p.err, ekey);
-      int j = NB - 1;
+        for (int b = 0; b < NB; ++b) {
+          load_own(b);
+          acc = add_rn(acc, Tree<T, W>::sum(cur));  // sequential running sums (kernels.py:221-223)
+          S[b] = acc;
+        }
+        const T total = acc;
+        uint64_t ka, kb;
+        unsigned long long ekey;
+        int r;
+        int64_t zidx;
+        token_keys<T, MODE_ROWS>(p, own_tok, 0, W, ka, kb, ekey, r, zidx);
+        const T stop = make_stop<T>(p, zidx, total, ka, kb, true);
+        if (!(total > T(0))) atomicMin(p.err, ekey);
+        int j = NB - 1;
 #pragma unroll
-      for (int b = NB - 2; b >= 0; --b)
-        if (stop < S[b]) j = b;
-      const T prev = j > 0 ? S[j - 1] : T(0);
-      T high = S[j];
-      T cur[W];
-      const T* row = tile + ((size_t)j * 32 + own) * TS;
-#pragma unroll
-      for (int g = 0; g < W / E; ++g) {
-        T a[E];
-        load_seg_smem(a, row + g * E);
-#pragma unroll
-        for (int e = 0; e < E; ++e) cur[g * E + e] = a[e];
+        for (int b = NB - 2; b >= 0; --b)
+          if (stop < S[b]) j = b;
+        if (NB > 1 && j != NB - 1) load_own(j);
+        T low = j > 0 ? S[j - 1] : T(0);
+        T high = S[j];
+        int lo = 0;
+        Walk<T, W / 2>::run(cur, low, high, stop, r, lo);
+        p.z[zidx] = j * W + lo;
       }
-      T low = prev;
-      int lo = 0;
-      Walk<T, W / 2>::run(cur, low, high, stop, r, lo);
-      p.z[zidx] = j * W + lo;
     }
     __syncwarp();  // every lane is done with this stage before it is refilled
   }

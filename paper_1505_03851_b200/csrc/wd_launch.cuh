@@ -260,8 +260,9 @@ int launch_draw(int variant, int W, int vec, int mode, const DrawParams<T>& p, v
       // K = W (fp32, W = 32): the single block staged in shared memory
       // (rows_stash_kernel; measured K = 32: 21.3 -> 27.4 G draws/s; staging
       // two blocks at K = 64 was slower than the per-row kernel, 15.9 vs 18.5)
-      // K = 32: the double-buffered variant (rows_stash2_kernel, measured
-      // 26.5 -> 27.9 G draws/s; at K = 64, two blocks per stage, 20.4 -> 18.6)
+      // K = 32: the double-buffered own-row variant (rows_stash2_kernel,
+      // measured 26.5 -> 31.1 G draws/s; at K = 64, two blocks per stage,
+      // 20.4 -> 19.5: not used)
       if (vec && W == 32 && p.K == 32) {
         if (WD_STASH2 & 1) return launch_rows_stash<T, 32, 1, 2>(p, st);
         return launch_rows_stash<T, 32, 1>(p, st);
