@@ -3,23 +3,31 @@
 standalone-sampler line and the CPU baselines), one JSON line on rank 0.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--scaling strong|weak]
     torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
 
-Workload (BASELINE.json configs[3] per GPU, weak scaling): a synthetic
-Wikipedia-shaped shard of 1M documents per GPU (lengths ~ Poisson(200),
-floor 1; words uniform over V = 40,000), K = 1024 topics, fp32, W = 32.
-One step = one full uncollapsed Gibbs iteration on the device: butterfly z
-draw with fused word-topic counts, NCCL all-reduce of the counts (N > 1),
-phi and theta Dirichlet resample.  Inputs (theta 4.1 GB, words 0.8 GB,
-phi 164 MB per GPU) exceed the 126 MB L2, so no flush is needed between steps.
+Workload (BASELINE.json configs[3]): a synthetic Wikipedia-shaped corpus of
+1M documents (lengths ~ Poisson(200), floor 1; words uniform over V =
+40,000), K = 1024 topics, fp32, W = 32.  --scaling strong (default): the
+SAME corpus is generated on every rank and document-sharded across the N
+GPUs (32-aligned, token-balanced cuts, sharding.shard_ranges) -- configs[3]
+as written.  --scaling weak: 1M documents per GPU.  One step = one full
+uncollapsed Gibbs iteration on the device: butterfly z draw with fused
+word-topic counts, NCCL all-reduce of the counts per vocabulary tile (N > 1),
+phi and theta Dirichlet resample.  Inputs (theta 4.1 GB, words 0.8 GB, phi
+164 MB at N = 1) exceed the 126 MB L2, so no flush is needed between steps.
 
-value  = all ranks' tokens / (max-over-ranks device time per step)
-e2e    = the same iteration entered from HOST buffers each step (pinned
-         H2D of offsets, words, theta, phi; D2H of z), i.e. the drop-in
-         draw_z / gibbs_iterate call with host data.
-roofline: the dominant kernel (bfly_kernel), algorithmic bytes per token
-         4K + 4K/Nbar + 8, averaged CUDA-event time of
-         its launches inside the timed region.
+value    = all ranks' tokens / (max-over-ranks device time per step)
+roofline = the dominant kernel (the butterfly LDA draw): algorithmic bytes
+           per token 4K + 4K/Nbar + 8 x tokens / its
+           CUDA-event time, against the L2 read ceiling measured in this
+           process (wd_l2_read_probe): the phi gathers are served from L2 by
+           design (vocabulary tiles), so L2 -> SM bandwidth is the roof.
+e2e      = the same iteration entered from HOST parameters each step
+           (DeviceLDA.iterate_from_host: pinned H2D of theta and phi, D2H of z).
+e2e_dropin = the reference-signature call draw_z("butterfly", N, theta, phi,
+           w, config, stops) with host numpy in and ragged int64 lists out, at
+           configs[2] size (1M docs, K = 200), wall clock per call.
 """
 
 from __future__ import annotations
@@ -46,13 +54,20 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--topics", type=int, default=1024)
-    ap.add_argument("--docs-per-gpu", type=int, default=1_000_000)
+    ap.add_argument("--docs", type=int, default=1_000_000,
+                    help="corpus size: total (strong scaling) or per GPU (weak scaling)")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
     ap.add_argument("--vocab", type=int, default=40_000)
     ap.add_argument("--mean-len", type=float, default=200.0)
     ap.add_argument("--seed", type=int, default=2026)
     ap.add_argument("--rows", type=int, default=1 << 20, help="standalone sampler rows (configs[1])")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample time")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dropin", action="store_true")
+    ap.add_argument("--dropin-docs", type=int, default=1_000_000)
+    ap.add_argument("--dropin-topics", type=int, default=200)
+    ap.add_argument("--no-python-ref", action="store_true",
+                    help="--impl reference: skip timing the reference's own Python draw_z_butterfly")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sampler", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
@@ -136,11 +151,31 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ corpus
-def make_shard(torch, rank, args, device):
-    """One GPU's document shard; padded with empty documents to a multiple of
-    32 (Corpus.padded, lda.py:56-63) so shards stay 32-aligned."""
-    g = torch.Generator(device=device).manual_seed(args.seed * 1000 + rank)
-    M = args.docs_per_gpu
+def workload_config(args, world):
+    """The workload both arms name (identical dicts: the reference arm runs a
+    bounded sample of exactly this workload)."""
+    return {
+        "workload": f"lda_cfg4_k{args.topics}",
+        "scaling": args.scaling,
+        "docs_total": args.docs * (world if args.scaling == "weak" else 1),
+        "vocab": args.vocab,
+        "topics": args.topics,
+        "mean_doc_len": args.mean_len,
+        "word_dist": "uniform",
+        "kernel": "butterfly",
+        "lanes": 32,
+        "parallelism": f"dp{world} (32-aligned, token-balanced document shards)",
+        "step": "draw z (+fused word_topic counts; N>1: NCCL all-reduce per vocabulary tile, overlapping the next "
+                "tile's draw) -> theta, phi resample",
+        "l2": "inputs larger than L2 (theta 4.1 GB, words 0.8 GB, phi 164 MB at N=1 vs 126 MB L2); no flush",
+    }
+
+
+def make_corpus(torch, seed, M, args, device):
+    """Synthetic corpus: lengths ~ Poisson(mean) floor 1, words uniform over V,
+    padded with empty documents to a multiple of 32 (Corpus.padded,
+    lda.py:56-63).  Deterministic in `seed` on any device."""
+    g = torch.Generator(device=device).manual_seed(seed)
     lengths = torch.poisson(torch.full((M,), args.mean_len, device=device), generator=g).clamp_(min=1).long()
     if M % 32:
         lengths = torch.cat([lengths, torch.zeros(32 - M % 32, dtype=torch.long, device=device)])
@@ -152,11 +187,38 @@ def make_shard(torch, rank, args, device):
     return off, words
 
 
+def make_shard(torch, rank, world, args, device):
+    """This rank's shard: (local offsets, local words, global doc of local doc 0).
+
+    strong: the same args.docs-document corpus on every rank (same generator),
+    cut by sharding.shard_ranges (32-aligned, balanced by tokens); rank r keeps
+    documents [lo, hi) with doc_base = lo, so z is the single-GPU run's.
+    weak: args.docs documents per rank (seed + rank), doc_base = rank x M."""
+    from paper_1505_03851_b200.sharding import shard_ranges
+
+    if args.scaling == "weak":
+        off, words = make_corpus(torch, args.seed * 1000 + rank, args.docs, args, device)
+        return off, words, rank * (off.numel() - 1)
+    off, words = make_corpus(torch, args.seed * 1000, args.docs, args, device)
+    lo, hi = shard_ranges(torch.diff(off).cpu().numpy(), world)[rank]
+    a, b = int(off[lo].item()), int(off[hi].item())
+    return (off[lo:hi + 1] - a).contiguous(), words[a:b].contiguous(), lo
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_sample_lda(args, theta_rows, phi_host, off_host, words_host, target_s):
     """Time the oracle (C port of the reference butterfly draw) on a doc sample
     with every host core; returns (tokens/s, cores, description)."""
-    import numpy as np
-
     from oracle import oracle as O
 
     cores = len(os.sched_getaffinity(0))
@@ -181,14 +243,73 @@ def cpu_sample_lda(args, theta_rows, phi_host, off_host, words_host, target_s):
     S1 = max(32, (S // max(1, cores)) // 32 * 32)
     dt1, ntok1 = run(S1, threads=1)
     return ntok / dt, cores, (f"draw_z butterfly fp32 W=32 K={args.topics} on {S} docs ({ntok} tokens) of the "
-                              f"same synthetic shard, oracle/wd_oracle.c C port, {cores} threads, {dt:.1f}s; "
+                              f"same synthetic corpus, oracle/wd_oracle.c C port, {cores} threads, {dt:.1f}s; "
                               f"1 thread: {ntok1 / dt1:.4g} tokens/s on {S1} docs"), ntok1 / dt1
 
 
 # --------------------------------------------------------------- reference
+def _reference_package():
+    """The unmodified reference, pip-installed into baseline/_ref (travels to
+    the GPU box), or the source tree in the build container."""
+    for cand in (os.environ.get("WARPDRAW_REF"), os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if cand and os.path.isdir(os.path.join(cand, "warpdraw")):
+            return cand
+    return None
+
+
+def _python_ref_worker(job):
+    """One process: the reference's own draw_z_butterfly (kernels.py:487-539,
+    the lockstep warp emulator) on one 32-document group."""
+    ref, K, V, mean, seed, idx = job
+    sys.path.insert(0, ref)
+    import numpy as np
+    from warpdraw.kernels import SeededStops, draw_z_butterfly
+    from warpdraw.warp import WarpConfig
+
+    g = np.random.default_rng(seed + idx)
+    N = np.maximum(g.poisson(mean, size=32), 1).astype(np.int64)
+    w = [g.integers(0, V, size=int(n)) for n in N]
+    theta = g.uniform(0.1, 1.0, size=(32, K)).astype(np.float32)
+    phi = g.uniform(0.1, 1.0, size=(V, K)).astype(np.float32)
+    t0 = time.perf_counter()
+    draw_z_butterfly(N, theta, phi, w, WarpConfig(32, 4), SeededStops(seed))
+    return int(N.sum()), time.perf_counter() - t0
+
+
+def python_reference(args, cores):
+    """the reference's own draw_z_butterfly (fp32, W = 32,
+    SeededStops) on 1 process and on C processes (multiprocessing, disjoint
+    32-document groups; do not use threads=, it is GIL-bound)."""
+    import multiprocessing as mp
+
+    ref = _reference_package()
+    if ref is None:
+        return {"unavailable": "reference package not installed under baseline/_ref"}
+    job = (ref, args.topics, args.vocab, args.mean_len, args.seed, 0)
+    ntok1, dt1 = _python_ref_worker(job)
+    procs = max(1, cores)
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(procs) as pool:
+        res = pool.map(_python_ref_worker, [job[:-1] + (i,) for i in range(procs)])
+    wall = time.perf_counter() - t0
+    ntok = sum(r[0] for r in res)
+    return {"single_process_tokens_per_s": ntok1 / dt1, "processes": procs,
+            "multiprocess_tokens_per_s": ntok / wall,
+            "sample": f"warpdraw.kernels.draw_z_butterfly (reference, {ref}) fp32 W=32 K={args.topics} V={args.vocab}:"
+                      f" one 32-document group (Poisson({args.mean_len:g})) per process; 1 process {ntok1} tokens in "
+                      f"{dt1:.1f}s; {procs} processes {ntok} tokens in {wall:.1f}s wall"}
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the reference path on the host cores (oracle C port of
-    draw_z_butterfly; the Python reference itself cannot travel to the box)."""
+    """--impl reference: the reference path on the host cores (rank 0 only).
+
+    value = the oracle C port of the reference's draw_z_butterfly
+    (oracle/wd_oracle.c: the reference algorithm restated in C, bit-exact with
+    it) on all host threads, each step a bounded document sample of the same
+    workload, draw only (the GPU arm's step also resamples, so the ratio is
+    conservative).  python_reference = the reference's own Python emulator
+    timed beside it (1 process and C processes)."""
     if rank != 0:
         return
     import numpy as np
@@ -201,7 +322,6 @@ def run_reference(args, rank, world):
     phi = rng.uniform(0.1, 1.0, size=(V, K)).astype(np.float32)
     # calibrate the per-step document sample to ~2 s of all-core work
     S = 256
-    lengths = np.maximum(rng.poisson(args.mean_len, size=S), 1)
     for _ in range(6):
         lengths = np.maximum(rng.poisson(args.mean_len, size=S), 1)
         off = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
@@ -224,20 +344,121 @@ def run_reference(args, rank, world):
     per = sum(times) / len(times)
     value = ntok / per
     sample = (f"draw_z butterfly fp32 W=32 K={K}, V={V}, {S} docs / {ntok} tokens per step "
-              f"(Poisson({args.mean_len:g}) lengths), oracle/wd_oracle.c C port of the reference algorithm")
+              f"(Poisson({args.mean_len:g}) lengths) of the workload, oracle/wd_oracle.c C port of the reference "
+              f"algorithm, {cores} threads, draw only")
+    pyref = None if args.no_python_ref else python_reference(args, cores)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        # the same workload as the GPU arm; each step is a bounded document
-        # sample of it (cpu_baseline.sample), draw only (no resample)
-        "config": {"workload": f"lda_cfg4_k{K}", "docs_per_gpu": args.docs_per_gpu, "vocab": V, "topics": K,
-                   "mean_doc_len": args.mean_len, "kernel": "butterfly", "lanes": 32,
-                   "parallelism": "host cores (rank 0 only)", "sample_docs_per_step": S},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample,
+                         "cpu_model": cpu_model()},
+        "python_reference": pyref,
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------- measurement
+def l2_read_peak(torch, dev):
+    """L2 -> SM read ceiling measured in this process (wd_l2_read_probe: 256-bit
+    ld.global.cg sweeps over a 40 MB L2-resident buffer, best grid size)."""
+    from paper_1505_03851_b200 import _lib
+
+    L = _lib.load()
+    sink = torch.zeros(1, device=dev)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    st = torch.cuda.current_stream()
+    best, best_cfg = 0.0, None
+    for mb in (24, 32, 40):
+        nbytes = mb << 20
+        buf = torch.rand(nbytes // 4, device=dev)
+        for blocks in (sms * 4, sms * 8, sms * 16):
+            _lib.check(L.wd_l2_read_probe(buf.data_ptr(), nbytes, 2, blocks, sink.data_ptr(), st.cuda_stream),
+                       "probe")
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 200
+            a.record(st)
+            _lib.check(L.wd_l2_read_probe(buf.data_ptr(), nbytes, reps, blocks, sink.data_ptr(), st.cuda_stream),
+                       "probe")
+            b.record(st)
+            torch.cuda.synchronize()
+            gbs = L.wd_l2_probe_bytes(nbytes, blocks) * reps / (a.elapsed_time(b) / 1e3) / 1e9
+            if gbs > best:
+                best, best_cfg = gbs, (mb, blocks)
+        del buf
+    return best, best_cfg
+
+
+def git_head():
+    try:
+        return subprocess.run(["git", "-C", ROOT, "rev-parse", "--short=12", "HEAD"], capture_output=True,
+                              text=True, timeout=5).stdout.strip() or None
+    except Exception:
+        return None
+
+
+def run_dropin(args, torch, dev):
+    """e2e_dropin: the reference-signature draw_z (kernels.py:542-555) with host
+    numpy theta/phi and ragged word lists in, ragged int64 z lists out, at
+    configs[2] size.  The first call converts and uploads the corpus (cached
+    per word-list object, as gibbs_iterate passes the same corpus.words every
+    iteration); later calls move theta, phi H2D and z D2H every call."""
+    import numpy as np
+
+    import paper_1505_03851_b200 as wd
+    from paper_1505_03851_b200 import kernels as KKt
+    from paper_1505_03851_b200.kernels import csr_to_ragged
+
+    M, K, V = args.dropin_docs, args.dropin_topics, args.vocab
+    off_d, words_d = make_corpus(torch, args.seed * 1000 + 77, M, args, dev)
+    off = off_d.cpu().numpy()
+    M = off.size - 1
+    N = np.diff(off)
+    w = csr_to_ragged(words_d.cpu().numpy().astype(np.int64), off)
+    g = torch.Generator(device=dev).manual_seed(args.seed + 5)
+    theta = (torch.rand((M, K), generator=g, device=dev) * 0.9 + 0.1).cpu().numpy()
+    phi = (torch.rand((V, K), generator=g, device=dev) * 0.9 + 0.1).cpu().numpy()
+    del off_d, words_d
+    cfg = wd.WarpConfig(32, 4)
+    t0 = time.perf_counter()
+    z = wd.draw_z("butterfly", N, theta, phi, w, cfg, wd.SeededStops(wd.derive_seed(args.seed, 1, 0)))
+    cold = time.perf_counter() - t0
+    del z
+    walls = []
+    for t in range(1, 4):
+        t0 = time.perf_counter()
+        z = wd.draw_z("butterfly", N, theta, phi, w, cfg, wd.SeededStops(wd.derive_seed(args.seed, 1, t)))
+        walls.append(time.perf_counter() - t0)
+        del z
+    warm = statistics.median(walls)
+    phases = {k: round(v * 1e3, 2) for k, v in KKt.last_host_timing.items()}
+    # the device draw alone on the same inputs (CUDA events), to split the wall time
+    from paper_1505_03851_b200 import kernels as KK
+
+    corpus = KK._host_corpora.get(N, w)
+    th = KK.to_block_aligned(torch.from_numpy(theta).to(dev))
+    ph = KK.to_block_aligned(torch.from_numpy(phi).to(dev))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    zd = wd.draw_z_device("butterfly", corpus, th, ph, wd.SeededStops(5), 32, check=False,
+                          err=torch.empty((1, 2), dtype=torch.int64, device=dev))
+    b.record()
+    torch.cuda.synchronize()
+    draw_s = a.elapsed_time(b) / 1e3
+    T = int(off[-1])
+    KK._host_corpora.clear()
+    KK._host_bufs.clear()
+    del th, ph, zd, corpus
+    return {"value": T / warm, "unit": "tokens/s", "h2d_bytes_per_step": int(theta.nbytes + phi.nbytes),
+            "d2h_bytes_per_step": int(4 * T), "ms_per_call": warm * 1e3, "first_call_ms": cold * 1e3,
+            "device_draw_ms": draw_s * 1e3, "host_overhead_ms": (warm - draw_s) * 1e3,
+            "phases_ms_last_call": phases,
+            "config": {"workload": f"lda_cfg3_k{K} (configs[2])", "docs": M, "tokens": T, "vocab": V, "topics": K},
+            "path": "paper_1505_03851_b200.draw_z('butterfly', N, theta, phi, w, WarpConfig(32, 4), "
+                    "SeededStops(...)): host numpy theta/phi + list of int64 word arrays -> list of int64 z "
+                    "arrays; wall clock per call (median of 3 after the first)"}
 
 
 # -------------------------------------------------------------------- ours
@@ -249,7 +470,6 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -262,18 +482,31 @@ def main():
     if world > 1 or args.force_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
+        # communicator lines (nranks, NVLS / P2P transport) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries only the JSON line
         dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
         pg = dist.group.WORLD
     K, V = args.topics, args.vocab
-    peak, peak_src = load_peaks()
+    hbm_peak, hbm_src = load_peaks()
 
-    off, words = make_shard(torch, rank, args, dev)
-    doc_base = rank * (off.numel() - 1)
+    off, words, doc_base = make_shard(torch, rank, world, args, dev)
     dcorpus = wd.DeviceCorpus.from_csr(off, words, doc_base=doc_base, vocab_size=V)
+    del words
     n_tok = dcorpus.n_tokens
     lda = DeviceLDA(dcorpus, K, V, lanes=32, seed=args.seed, process_group=pg)
-    g = torch.Generator(device=dev).manual_seed(args.seed + 7919 * rank)
-    lda.theta.uniform_(0.1, 1.0, generator=g)
+    g = torch.Generator(device=dev).manual_seed(args.seed + 7919 * (rank if args.scaling == "weak" else 0))
+    if args.scaling == "weak":
+        lda.theta.uniform_(0.1, 1.0, generator=g)
+    else:  # theta rows of the global corpus: rank r's block of the same matrix
+        for lo in range(0, doc_base + dcorpus.n_docs, 1 << 18):
+            hi = min(lo + (1 << 18), doc_base + dcorpus.n_docs)
+            blk = torch.empty((hi - lo, K), device=dev).uniform_(0.1, 1.0, generator=g)
+            a, b = max(lo, doc_base), hi
+            if b > a:
+                lda.theta[a - doc_base:b - doc_base].copy_(blk[a - lo:b - lo])
+            del blk
     g = torch.Generator(device=dev).manual_seed(args.seed)  # phi identical on every rank
     lda.phi.uniform_(0.1, 1.0, generator=g)
     stream = torch.cuda.current_stream()
@@ -286,6 +519,7 @@ def main():
         lda.iterate(t)
     torch.cuda.synchronize()
     lda.check_errors()
+    l2_peak, l2_cfg = l2_read_peak(torch, dev)
     barrier()
     torch.cuda.synchronize()
 
@@ -297,7 +531,6 @@ def main():
     e_start.record(stream)
     for s in range(args.steps):
         t = args.warmup + s
-        lda.word_topic.zero_()
         d_ev[s][0].record(stream)
         lda.draw(t, overlap_allreduce=True)  # per-tile count all-reduce behind each tile (N > 1)
         d_ev[s][1].record(stream)
@@ -315,27 +548,24 @@ def main():
     if pg is not None:
         dist.all_reduce(red, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-    elapsed, draw_avg = float(red[0]), float(red[1])
+    elapsed_max, draw_max = float(red[0]), float(red[1])
     total_tokens = float(tot[0])
-    per_step = elapsed / args.steps
+    per_step = elapsed_max / args.steps
     value = total_tokens / per_step
-    nbar = n_tok / dcorpus.n_docs
+    nbar = n_tok / max(1, dcorpus.n_docs)
     bytes_per_tok = 4 * K + 4 * K / nbar + 8
+    # rank 0's own draw (its tokens / its CUDA-event time): the kernel's rate
     achieved = n_tok * bytes_per_tok / draw_avg / 1e9
     n_draw = lda.tiles.n_tiles if lda.tiles is not None else 1
     launches_per_step = n_draw + 5 + 1  # draw (per vocab tile) + phi (3 passes + 2 col reductions) + theta
 
     # ---------------------------------------------------------------- e2e
     # The same iteration entered from HOST parameters every step, as a caller
-    # of gibbs_iterate(corpus, params, ...) with numpy theta/phi would: pinned
+    # of gibbs_iterate(corpus, params, ...) with host theta/phi would: pinned
     # H2D of theta and phi, the device iteration, D2H of z.  The corpus is
     # static across iterations and stays resident (uploaded once per Corpus).
     e2e = None
     if not args.no_e2e:
-        # DeviceLDA.iterate_from_host: inputs of step s+1 are copied (pinned
-        # H2D, copy stream) while step s computes, and z of step s returns
-        # (D2H, second copy stream) while step s+1 computes: the prefetching
-        # a data loader does.  Every step moves its full inputs and result.
         h_theta = lda.theta.cpu().pin_memory()
         h_phi = lda.phi.cpu().pin_memory()
         # z returns as int16 when K <= 32767 (exact; cast on the device, half the D2H bytes)
@@ -361,7 +591,7 @@ def main():
                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(et[0]) * 1e3,
                "path": "DeviceLDA.iterate_from_host: pinned host theta/phi -> Gibbs iteration on the resident "
                        "corpus -> z (int16) to host (next step's H2D and previous step's D2H overlap the "
-                       "current step; bound by H2D, which shares L2 with the L2-bound draw)"}
+                       "current step)"}
         del h_theta, h_phi, h_z
         lda._host_pipe = None
 
@@ -386,22 +616,31 @@ def main():
                 wd.sample_rows(wts, 5, variant=var, out=out, err=err, check=False)
             b.record(stream)
             torch.cuda.synchronize()
-            dt = a.elapsed_time(b) / 1e3 / 10
-            res[var] = dt
+            res[var] = a.elapsed_time(b) / 1e3 / 10
         bpd = 4 * K + 4
         sampler = {
-            "workload": f"standalone rows n={n} K={K} fp32 W=32 (configs[1])",
+            "workload": f"standalone rows n={n} K={K} fp32 W=32 (configs[1]), weights 4.3 GB > L2",
             "draws_per_s": n / res["butterfly"],
-            "roofline_frac": n * bpd / res["butterfly"] / 1e9 / peak,
+            "roofline": {"bound": "hbm", "achieved": n * bpd / res["butterfly"] / 1e9, "peak": hbm_peak,
+                         "peak_source": hbm_src, "unit": "GB/s",
+                         "frac": n * bpd / res["butterfly"] / 1e9 / hbm_peak, "bytes_per_draw": bpd},
             "prefix_table_draws_per_s": n / res["prefix"],
             "speedup_vs_prefix_table": res["prefix"] / res["butterfly"],
         }
-        del wts
+        del wts, out
+
+    del lda
+    torch.cuda.empty_cache()
+
+    # ------------------------------------------------- e2e drop-in (configs[2])
+    dropin = None
+    if rank == 0 and world == 1 and not args.no_dropin:
+        dropin = run_dropin(args, torch, dev)
 
     # ------------------------------------------------------- CPU baseline
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        S_max = dcorpus.n_docs
+        S_max = min(dcorpus.n_docs, 200_000)
         th = (torch.rand((S_max, K), generator=torch.Generator(device=dev).manual_seed(1), device=dev) * 0.9
               + 0.1).cpu().numpy()
         # synth_params-style positive theta/phi (bench.py:187-192 of the
@@ -409,17 +648,16 @@ def main():
         # full of subnormals that would slow the CPU port ~3x
         ph = (torch.rand((V, K), generator=torch.Generator(device=dev).manual_seed(2), device=dev) * 0.9
               + 0.1).cpu().numpy()
-        v, cores, desc, v1 = cpu_sample_lda(args, th, ph, off[: S_max + 1].cpu().numpy(), words.cpu().numpy(),
+        v, cores, desc, v1 = cpu_sample_lda(args, th, ph, dcorpus.offsets[: S_max + 1].cpu().numpy(),
+                                            dcorpus.words[: int(dcorpus.offsets[S_max])].cpu().numpy(),
                                             args.cpu_seconds)
         cpu = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc,
-               "single_core_value": v1}
+               "single_core_value": v1, "cpu_model": cpu_model()}
 
     ncu = ncu_summary()
-    l2_bytes = None
-    if K == 1024 and "bfly_lda_k1024" in ncu:
-        l2_bytes = ncu["bfly_lda_k1024"].get("lts_tex_read_bytes_per_draw") or ncu["bfly_lda_k1024"].get(
-            "lts_bytes_per_draw")
+    nk = ncu.get(f"bfly_lda_k{K}") if args.scaling == "strong" or world == 1 else None
     if rank == 0:
+        cfg = workload_config(args, world)
         line = {
             "metric": METRIC,
             "value": value,
@@ -429,61 +667,46 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": per_step * 1e3,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": args.scaling,
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic",
-            "config": {
-                "workload": f"lda_cfg4_k{K}",
-                "docs_per_gpu": args.docs_per_gpu,
-                "tokens_per_gpu": n_tok,
-                "vocab": V,
-                "topics": K,
-                "mean_doc_len": args.mean_len,
-                "kernel": "butterfly",
-                "lanes": 32,
-                "vocab_tiles": n_draw,
-                "step": "draw z (+fused word_topic counts; N>1: NCCL all-reduce per vocabulary tile, overlapping the next tile's draw) -> theta, phi resample",
-                "parallelism": f"dp{world} (32-aligned document shards)",
-                "l2": "inputs larger than L2 (theta 4.1 GB, words 0.8 GB, phi 164 MB per GPU vs 126 MB L2)",
-            },
+            "config": cfg,
+            "tokens_per_step": int(total_tokens),
+            "tokens_rank0": n_tok,
             "roofline": {
-                "bound": "hbm",
-                "kernel": "bfly_kernel<float,32,VEC,LDA>",
+                "bound": "l2",
+                "kernel": "bfly_kernel<float,32,VEC,LDA> (butterfly LDA draw, vocabulary-tiled)",
                 "achieved": achieved,
-                "peak": peak,
-                "peak_source": peak_src,
+                "peak": l2_peak,
+                "peak_source": "measured in this run: wd_l2_read_probe (256-bit ld.global.cg sweeps of an "
+                               "L2-resident buffer, best over 24/32/40 MB x 3 grid sizes; best at "
+                               f"{l2_cfg[0]} MB, {l2_cfg[1]} CTAs)",
                 "unit": "GB/s",
-                "frac": achieved / peak,
-                # per launch like `achieved` (which is the same ratio per draw):
-                # ncu dram read+write of the draw's vocabulary-tile launches / launches
-                "traffic": (ncu["bfly_lda_k1024"]["dram_bytes_per_draw"] / ncu["bfly_lda_k1024"]["launches_per_draw"]
-                            if K == 1024 and "bfly_lda_k1024" in ncu else None),
-                "traffic_unit": "bytes per launch (ncu dram read+write, mean over the vocabulary-tile launches)",
+                "frac": achieved / l2_peak,
+                "algorithmic_bytes_per_token": bytes_per_tok,
                 "algorithmic_bytes_per_launch": n_tok * bytes_per_tok / n_draw,
                 "launches_per_draw": n_draw,
-                "bytes_per_token": bytes_per_tok,
-                "note": "the phi gathers are served from L2 by design (vocabulary tiles keep each phi slice "
-                        "L2-resident), so algorithmic bytes / HBM peak exceeds 1; the binding roofline is "
-                        "roofline.l2 (SM L2 reads vs a streaming L2 read kernel); DRAM traffic = traffic",
                 "draw_ms": draw_avg * 1e3,
+                "draw_ms_max_over_ranks": draw_max * 1e3,
                 "draw_share_of_step": draw_avg / per_step,
-                # the phi gathers are served from L2 by design (vocabulary
-                # tiles): the binding roofline is the measured L2 read peak
-                "l2": ({"achieved_gbs": (l2_bytes / draw_avg / 1e9),
-                        "peak_gbs": ncu.get("l2_read_peak_gbs"),
-                        "frac": (l2_bytes / draw_avg / 1e9) / ncu["l2_read_peak_gbs"],
-                        "bytes_per_draw": l2_bytes,
-                        "note": "ncu L2 read bytes requested by the SMs per draw (lts__t_sectors_srcunit_tex_op_read"
-                                " x 32) / CUDA-event draw time; peak = streaming 256-bit L2 read kernel "
-                                "(tools/l2_peak.py)"}
-                       if l2_bytes and ncu.get("l2_read_peak_gbs") else None),
+                # DRAM bytes per launch from the committed ncu capture of this
+                # workload (N = 1 shape); the phi gathers hit L2 by design
+                "traffic": (nk["dram_bytes_per_draw"] / nk["launches_per_draw"]) if nk else None,
+                "traffic_unit": "bytes per launch (ncu dram read+write, mean over the vocabulary-tile launches)",
+                "traffic_capture": ({"file": "profiles/ncu_summary.json", "head": nk.get("head"),
+                                     "source": nk.get("source")} if nk else None),
+                "hbm": ({"dram_gbs": nk["dram_bytes_per_draw"] / draw_avg / 1e9, "peak": hbm_peak,
+                         "peak_source": hbm_src, "frac": nk["dram_bytes_per_draw"] / draw_avg / 1e9 / hbm_peak}
+                        if nk and world == 1 else None),
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_dropin": dropin,
             "clocks": clk,
             "gpu_launches": launches_per_step * args.steps,
             "sampler": sampler,
+            "head": git_head(),
         }
         print(json.dumps(line), flush=True)
     if pg is not None:

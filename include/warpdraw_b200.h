@@ -159,9 +159,9 @@ int wd_topic_counts(const int32_t* words, const int32_t* token_doc, const int32_
 
 /*
  * Throughput-mode Dirichlet resample (lda.py:185-208), statistical parity:
- * Gammas from a counter-based stream (32-bit integer hash of a counter)
- * keyed by (seed, row, topic, attempt), Marsaglia-Tsang in log space,
- * deterministic reductions.
+ * every Gamma attempt is one Philox4x32-10 block of counter (row lo, row hi,
+ * topic, attempt) under the 64-bit iteration seed, Marsaglia-Tsang in log
+ * space, deterministic reductions.
  *   wd_resample_theta: theta[m, :] ~ Dir(alpha + histogram of z over doc m)
  *     (the doc-topic counts are formed in shared memory, never in HBM);
  *     row key = doc_base + m.
@@ -169,6 +169,13 @@ int wd_topic_counts(const int32_t* words, const int32_t* token_doc, const int32_
  *     [vocab_size x n_topics] int32 (dense, ld = n_topics); scratch of
  *     wd_resample_phi_workspace_bytes(n_topics) bytes.
  */
+/* The Gamma stream of the resample kernels, cell by cell: out[i] = log of
+ * the Gamma(shapes[i], 1) draw the resample kernels make for (rows[i],
+ * topics[i]) under `seed` (same attempts, same arithmetic).  Test/KAT entry
+ * (replaces numpy's Generator.gamma at lda.py:201-205). */
+int wd_log_gamma_draws(uint64_t seed, const int64_t* rows, const int32_t* topics, const float* shapes,
+                       int64_t n, float* out, void* stream);
+
 int wd_resample_theta(int dtype, const int32_t* z, const int64_t* doc_offsets, int64_t n_docs,
                       int32_t n_topics, double alpha, uint64_t seed, int64_t doc_base, void* theta,
                       int64_t ld_theta, void* stream);
@@ -210,6 +217,15 @@ size_t wd_stream_workspace_bytes(int64_t n_draws);
 int wd_stream_draws(int method, const double* table, const uint64_t* thresh, const int32_t* alias,
                     int64_t n_weights, uint64_t seed, int64_t n_draws, int32_t* out, void* workspace,
                     size_t workspace_bytes, void* stream);
+
+/*
+ * Measurement (no reference counterpart): the L2 -> SM read ceiling the
+ * vocabulary-tiled LDA draw runs against.  `reps` grid-stride sweeps of
+ * 256-bit ld.global.cg loads over a 32-byte-aligned, L2-resident buffer;
+ * wd_l2_probe_bytes(buffer_bytes, blocks) = bytes read per sweep.
+ */
+int64_t wd_l2_probe_bytes(int64_t buffer_bytes, int blocks);
+int wd_l2_read_probe(const void* buffer, int64_t buffer_bytes, int reps, int blocks, float* sink, void* stream);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,6 @@ from .samplers import (
     sample_rows,
 )
 from .sampling import AllZeroError, EmptyWeightsError
-from .warp import Trace, WarpConfig
+from .warp import OutOfBoundsError, Trace, WarpConfig
 
 __version__ = "0.1.0"

@@ -33,6 +33,7 @@ EXPORTS = (
     "wd_sample_rows",
     "wd_units",
     "wd_topic_counts",
+    "wd_log_gamma_draws",
     "wd_resample_theta",
     "wd_resample_phi_workspace_bytes",
     "wd_resample_phi",
@@ -40,6 +41,8 @@ EXPORTS = (
     "wd_prefix_f64",
     "wd_stream_workspace_bytes",
     "wd_stream_draws",
+    "wd_l2_probe_bytes",
+    "wd_l2_read_probe",
 )
 
 
@@ -74,6 +77,8 @@ def _declare(L):
     L.wd_topic_counts.restype = i32
     L.wd_topic_counts.argtypes = [vp, vp, vp, i64, ctypes.c_int32, vp, vp, vp]
     dbl = ctypes.c_double
+    L.wd_log_gamma_draws.restype = i32
+    L.wd_log_gamma_draws.argtypes = [u64, vp, vp, vp, i64, vp, vp]
     L.wd_resample_theta.restype = i32
     L.wd_resample_theta.argtypes = [i32, vp, vp, i64, ctypes.c_int32, dbl, u64, i64, vp, i64, vp]
     L.wd_resample_phi_workspace_bytes.restype = sz
@@ -88,6 +93,10 @@ def _declare(L):
     L.wd_stream_workspace_bytes.argtypes = [i64]
     L.wd_stream_draws.restype = i32
     L.wd_stream_draws.argtypes = [i32, vp, vp, vp, i64, u64, i64, vp, vp, sz, vp]
+    L.wd_l2_probe_bytes.restype = i64
+    L.wd_l2_probe_bytes.argtypes = [i64, i32]
+    L.wd_l2_read_probe.restype = i32
+    L.wd_l2_read_probe.argtypes = [vp, i64, i32, i32, vp, vp]
 
 
 def load(path: str | None = None):

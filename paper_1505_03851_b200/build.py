@@ -23,10 +23,43 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.environ.get("WD_LIB_OUT") or os.path.join(OUT_DIR, "libwarpdraw_b200.so")
-SOURCES = ["wd_draw_f32.cu", "wd_draw_f64.cu", "wd_capi.cu", "wd_resample.cu", "wd_stream.cu"]
+SOURCES = ["wd_draw_f32.cu", "wd_draw_f64.cu", "wd_capi.cu", "wd_resample.cu", "wd_stream.cu", "wd_probe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # sources whose results are statistical (device resample, log-likelihood)
 STATISTICAL_SOURCES = {"wd_resample.cu"}
+
+
+HOST_SRC = os.path.join(CSRC, "wd_host.c")
+
+
+def host_ext_path() -> str:
+    import sysconfig
+
+    return os.path.join(PKG, "_wdhost" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_host(force: bool = False) -> str:
+    """The CPython host helper (_wdhost: ragged <-> CSR loops of the drop-in
+    boundary), compiled with the system C compiler against this interpreter's
+    and numpy's headers."""
+    import sysconfig
+
+    import numpy as np
+
+    out = host_ext_path()
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(HOST_SRC):
+        return out
+    cc = os.environ.get("CC") or shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        raise RuntimeError("no C compiler for the host helper")
+    tmp = out + ".tmp"
+    cmd = [cc, "-O2", "-shared", "-fPIC", "-std=c11", "-Wall", f"-I{sysconfig.get_paths()['include']}",
+           f"-I{np.get_include()}", HOST_SRC, "-o", tmp]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"host helper build failed:\n{r.stderr}")
+    os.replace(tmp, out)
+    return out
 
 
 def nvcc() -> str:
@@ -46,7 +79,8 @@ def _flags(ptxas_verbose: bool):
 
 
 def _deps():
-    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INCLUDE, "warpdraw_b200.h")]
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f != "wd_host.c"] + \
+        [os.path.join(INCLUDE, "warpdraw_b200.h")]
 
 
 def up_to_date() -> bool:
@@ -57,6 +91,7 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, ptxas_verbose: bool = False, verbose: bool = True) -> str:
+    build_host(force)
     if not force and up_to_date():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)

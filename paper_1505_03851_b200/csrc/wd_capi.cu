@@ -27,10 +27,17 @@ void set_last_cuda_error(cudaError_t e) {
 }
 
 int device_sm_count() {
-  int dev = 0, n = 0;
+  // queried once per device (cudaGetDevice is a cheap thread-local read)
+  constexpr int kMaxDev = 64;
+  static int cache[kMaxDev] = {0};
+  int dev = 0;
   cudaGetDevice(&dev);
+  if (dev >= 0 && dev < kMaxDev && cache[dev] > 0) return cache[dev];
+  int n = 0;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n > 0 ? n : 1;
+  n = n > 0 ? n : 1;
+  if (dev >= 0 && dev < kMaxDev) cache[dev] = n;
+  return n;
 }
 
 // --------------------------------------------------------- aux kernels

@@ -66,20 +66,27 @@ template <typename T> __device__ __forceinline__ T from_double(double u);
 template <> __device__ __forceinline__ float from_double<float>(double u) { return __double2float_rn(u); }
 template <> __device__ __forceinline__ double from_double<double>(double u) { return u; }
 
-// Opt-in Philox4x32-10 (WD_STOPS_PHILOX): counter (doc, key), key = seed.
-// Not reference-parity (SURVEY.md section 0 fact 5); 53-bit unit from 2 words.
-__device__ __forceinline__ uint64_t philox_bits(uint64_t seed, uint64_t a, uint64_t b) {
-  uint32_t c0 = (uint32_t)a, c1 = (uint32_t)(a >> 32), c2 = (uint32_t)b, c3 = (uint32_t)(b >> 32);
-  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+// Philox4x32-10 (Salmon et al., SC'11; Random123's constants): one 128-bit
+// block for a 128-bit counter under a 64-bit key.
+__device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                               uint32_t k1) {
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
-    uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-    uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
     c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
     k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
   }
-  return ((uint64_t)c0 << 21) | (uint64_t)(c1 >> 11);
+  return make_uint4(c0, c1, c2, c3);
+}
+
+// Opt-in Philox4x32-10 stops (WD_STOPS_PHILOX): counter (doc, key), key = seed.
+// Not reference-parity (SURVEY.md section 0 fact 5); 53-bit unit from 2 words.
+__device__ __forceinline__ uint64_t philox_bits(uint64_t seed, uint64_t a, uint64_t b) {
+  const uint4 r = philox4x32_10((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32), (uint32_t)seed,
+                                (uint32_t)(seed >> 32));
+  return ((uint64_t)r.x << 21) | (uint64_t)(r.y >> 11);
 }
 
 // ------------------------------------------------------------- L2 policies

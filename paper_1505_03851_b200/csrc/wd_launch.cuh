@@ -8,6 +8,7 @@
 #include <map>
 #include <type_traits>
 #include <mutex>
+#include <tuple>
 #include <utility>
 
 #include "wd_draw.cuh"
@@ -30,16 +31,21 @@ void set_last_cuda_error(cudaError_t e);
 
 inline int occupancy_blocks(const void* fn, size_t smem, int threads = kThreads) {
   static std::mutex mu;
-  static std::map<std::pair<const void*, size_t>, int> cache;
-  static std::map<const void*, size_t> smem_attr;  // per kernel: the largest opt-in set so far
+  // keyed by (device, function): cudaFuncSetAttribute applies to the current
+  // device only, and occupancy may differ between devices of one process
+  static std::map<std::tuple<int, const void*, size_t>, int> cache;
+  static std::map<std::pair<int, const void*>, size_t> smem_attr;  // largest opt-in set so far
+  int dev = 0;
+  cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
   // the opt-in dynamic shared memory limit is per function: only ever raise it
   // (a smaller request after a larger one must not lower it under a cached launch)
-  if (smem > 48 * 1024 && smem > smem_attr[fn]) {
+  auto fkey = std::make_pair(dev, fn);
+  if (smem > 48 * 1024 && smem > smem_attr[fkey]) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    smem_attr[fn] = smem;
+    smem_attr[fkey] = smem;
   }
-  auto key = std::make_pair(fn, smem * 1024 + (size_t)threads);
+  auto key = std::make_tuple(dev, fn, smem * 1024 + (size_t)threads);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int nb = 0;

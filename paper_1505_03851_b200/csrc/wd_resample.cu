@@ -8,8 +8,10 @@
 //
 // Statistical (not bitwise) parity: the reference draws its Gammas from
 // numpy's PCG64 stream, which has no device equivalent.  Here every Gamma
-// is drawn from a counter-based stream keyed by (seed, row, topic, attempt)
-// -- a 32-bit integer hash of the counter -- so the result is independent of
+// attempt is one Philox4x32-10 block: counter (global row lo, row hi, topic,
+// attempt), key = the 64-bit iteration seed -- a bijection of the full
+// 128-bit counter, so no two (row, topic, attempt) cells of one iteration
+// share their words at any corpus size, and the result is independent of
 // launch geometry and of the number of GPUs.  Marsaglia-Tsang
 // (shape < 1 boosted by U^(1/a)) is evaluated in LOG space, so the tiny
 // Gammas of alpha = 0.1 / beta = 0.01 shapes never underflow before
@@ -29,31 +31,24 @@ namespace wd {
 int device_sm_count();
 void set_last_cuda_error(cudaError_t e);
 
-// Four 32-bit words for attempt `ctr` of Gamma (row, k): a 32-bit integer
-// hash (lowbias32 finalizer) of a counter built from a per-row key, the topic
-// and the attempt -- single-instruction 32-bit multiplies, ~7 instructions
-// per word (the 64-bit SplitMix/Philox alternatives cost 3-4x more here).
-struct Rand4 {
-  uint32_t x, y, z, w;
+// The Gamma stream: attempt `ctr` of Gamma (row, k) is the Philox4x32-10
+// block of counter (row lo, row hi, k, ctr) under the iteration seed (128-bit
+// counter, 64-bit key: distinct cells never share words).  The previous
+// stream folded (row, topic) into one 32-bit hash, so at 1e9 cells per
+// iteration ~21% of the cells shared their uniforms with another cell.
+struct GammaRow {
+  uint32_t r0, r1, k0, k1;
 };
-__device__ __forceinline__ uint32_t hash32(uint32_t x) {
-  x ^= x >> 16;
-  x *= 0x7feb352du;
-  x ^= x >> 15;
-  x *= 0x846ca68bu;
-  x ^= x >> 16;
-  return x;
+__device__ __forceinline__ GammaRow gamma_row(uint64_t seed, uint64_t row) {
+  return {(uint32_t)row, (uint32_t)(row >> 32), (uint32_t)seed, (uint32_t)(seed >> 32)};
 }
-__device__ __forceinline__ uint32_t row_key(uint64_t seed, uint64_t row) {
-  return hash32((uint32_t)seed ^ hash32((uint32_t)row ^ hash32((uint32_t)(row >> 32) ^ (uint32_t)(seed >> 32))));
-}
-__device__ __forceinline__ Rand4 rand4(uint32_t rkey, uint32_t k, uint32_t ctr) {
-  const uint32_t base = hash32(rkey ^ (k * 0x9E3779B9u)) + ctr * 0x632BE5ABu;
-  return {hash32(base), hash32(base + 0x85EBCA6Bu), hash32(base + 0xC2B2AE35u), hash32(base + 0x27D4EB2Fu)};
+__device__ __forceinline__ uint4 rand4(const GammaRow& g, uint32_t k, uint32_t ctr) {
+  return philox4x32_10(g.r0, g.r1, k, ctr, g.k0, g.k1);
 }
 
-// uniform in (0, 1): 24-bit mantissa, never 0
-__device__ __forceinline__ float u01(uint32_t x) { return ((float)(x >> 8) + 0.5f) * 0x1p-24f; }
+// uniform in (0, 1) from all 32 bits: (x + 1/2) 2^-32, never 0 (rounded to
+// float: the resolution near 0 is 2^-33, so log U reaches -22.9)
+__device__ __forceinline__ float u01(uint32_t x) { return fmaf((float)x, 0x1p-32f, 0x1p-33f); }
 
 // One Marsaglia-Tsang attempt (2000) for log Gamma(a, 1) from the counter
 // block (row key, topic, attempt); shapes a < 1 use the boost Gamma(a) = Gamma(a + 1)
@@ -62,8 +57,8 @@ __device__ __forceinline__ float u01(uint32_t x) { return ((float)(x >> 8) + 0.5
 // Evaluated in LOG space so alpha = 0.1 / beta = 0.01 shapes never underflow.
 // SFU approximations (__logf, __cosf, rsqrtf, __fdividef; this file is
 // compiled with FMA contraction and flush-to-zero): statistical, not bitwise.
-__device__ __forceinline__ bool log_gamma_attempt(float a, uint32_t rkey, uint32_t k, uint32_t ctr, float& out) {
-  const Rand4 r = rand4(rkey, k, ctr);
+__device__ __forceinline__ bool log_gamma_attempt(float a, const GammaRow& g, uint32_t k, uint32_t ctr, float& out) {
+  const uint4 r = rand4(g, k, ctr);
   float boost = 0.f;
   if (a < 1.f) {
     boost = __fdividef(__logf(u01(r.w)), a);
@@ -124,7 +119,7 @@ __global__ void __launch_bounds__(256) theta_kernel(const int32_t* __restrict__ 
     // per-lane progress: a rejection costs that lane one more attempt instead
     // of stalling the whole warp at every topic (divergence only at the tail)
     uint32_t ctr = 0;
-    const uint32_t rkey = row_key(seed, row);
+    const GammaRow rkey = gamma_row(seed, row);
     for (int k = lane; k < K;) {
       float v;
       if (log_gamma_attempt(alpha + (float)hist[k], rkey, (uint32_t)k, ctr, v)) {
@@ -189,7 +184,7 @@ __global__ void __launch_bounds__(256) theta_kernel_wide(const int32_t* __restri
       }
     }
     __syncwarp();
-    const uint32_t rkey = row_key(seed, (uint64_t)(doc_base + m));
+    const GammaRow rkey = gamma_row(seed, (uint64_t)(doc_base + m));
     float mx = -INFINITY;
     uint32_t ctr = 0;
     for (int k = lane; k < K;) {
@@ -218,6 +213,18 @@ __global__ void __launch_bounds__(256) theta_kernel_wide(const int32_t* __restri
   }
 }
 
+// wd_log_gamma_draws: the per-cell attempt loop of the resample kernels.
+__global__ void log_gamma_cells(uint64_t seed, const int64_t* __restrict__ rows, const int32_t* __restrict__ topics,
+                                const float* __restrict__ shapes, int64_t n, float* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const GammaRow g = gamma_row(seed, (uint64_t)rows[i]);
+    float v;
+    uint32_t ctr = 0;
+    while (!log_gamma_attempt(shapes[i], g, (uint32_t)topics[i], ctr, v)) ++ctr;
+    out[i] = v;
+  }
+}
+
 // phi[:, k] ~ Dir(beta + word_topic[:, k]): three passes over V x K with
 // per-CTA column partials reduced in a fixed order (deterministic).
 constexpr int kPhiThreads = 256;
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(kPhiThreads) phi_pass(int pass, const int32_t*
     const float cs = pass == 0 ? 0.f : colstat[k];
     if (pass == 0) {
       uint32_t ctr = 0;
-      uint32_t rkey = row_key(seed, (uint64_t)v0);
+      GammaRow rkey = gamma_row(seed, (uint64_t)v0);
       for (int64_t v = v0; v < v1;) {
         float lgv;
         if (log_gamma_attempt(beta + (float)wt[v * (int64_t)K + k], rkey, (uint32_t)k, ctr, lgv)) {
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__(kPhiThreads) phi_pass(int pass, const int32_t*
           acc = fmaxf(acc, lgv);
           ++v;
           ctr = 0;
-          rkey = row_key(seed, (uint64_t)v);
+          rkey = gamma_row(seed, (uint64_t)v);
         } else {
           ++ctr;
         }
@@ -422,6 +429,15 @@ int wd_resample_theta(int dtype, const int32_t* z, const int64_t* doc_offsets, i
     return resample_theta_t<double>(z, doc_offsets, n_docs, n_topics, (float)alpha, seed, doc_base, (double*)theta,
                                     ld_theta, st);
   return WD_ERR_INVALID_ARGUMENT;
+}
+
+int wd_log_gamma_draws(uint64_t seed, const int64_t* rows, const int32_t* topics, const float* shapes, int64_t n,
+                       float* out, void* stream) {
+  if (n < 0 || (n > 0 && (!rows || !topics || !shapes || !out))) return WD_ERR_INVALID_ARGUMENT;
+  if (n == 0) return WD_OK;
+  int64_t want = (n + 255) / 256, cap = (int64_t)device_sm_count() * 16;
+  log_gamma_cells<<<(int)(want < cap ? want : cap), 256, 0, (cudaStream_t)stream>>>(seed, rows, topics, shapes, n, out);
+  return ck();
 }
 
 size_t wd_resample_phi_workspace_bytes(int32_t n_topics) {

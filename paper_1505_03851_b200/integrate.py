@@ -16,7 +16,7 @@ After install():
   samplers (bench.py:150-154), bit-identical, and SAMPLERS["prefix"] (the
   butterfly's u stream through a full prefix table) is added;
 * the reference's exception classes are the ones raised (AllZeroError,
-  StopOutOfRangeError are mapped), and its SeededStops / InjectedStops
+  EmptyWeightsError, StopOutOfRangeError, OutOfBoundsError are mapped, for draw_z and SAMPLERS), and its SeededStops / InjectedStops
   objects are recognised (in-kernel hash / u per token).
 
 uninstall() restores the originals.
@@ -28,6 +28,7 @@ import importlib
 
 from . import kernels as _k
 from . import samplers as _s
+from . import warp as _w
 
 _saved: dict = {}
 
@@ -44,6 +45,8 @@ def _convert(x, ref_kernels):
 
 
 def _wrap_errors(fn, ref_kernels, ref_sampling):
+    ref_warp = importlib.import_module(ref_kernels.__name__.rsplit(".", 1)[0] + ".warp")
+
     def call(*a, **kw):
         a = tuple(_convert(x, ref_kernels) for x in a)
         kw = {k: _convert(v, ref_kernels) for k, v in kw.items()}
@@ -53,6 +56,10 @@ def _wrap_errors(fn, ref_kernels, ref_sampling):
             raise ref_kernels.StopOutOfRangeError(str(exc)) from None
         except _k.AllZeroError as exc:
             raise ref_sampling.AllZeroError(str(exc)) from None
+        except _s.EmptyWeightsError as exc:
+            raise ref_sampling.EmptyWeightsError(str(exc)) from None
+        except _w.OutOfBoundsError as exc:
+            raise ref_warp.OutOfBoundsError(str(exc)) from None
 
     call.__name__ = getattr(fn, "__name__", "call")
     call.__doc__ = fn.__doc__
@@ -74,7 +81,7 @@ def install(package: str = "warpdraw") -> None:
     gpu_draw_z = _wrap_errors(_k.draw_z, ref_kernels, ref_sampling)
     ref_kernels.draw_z = gpu_draw_z
     ref_lda.draw_z = gpu_draw_z
-    ref_bench.SAMPLERS.update(_s.SAMPLERS)
+    ref_bench.SAMPLERS.update({name: _wrap_errors(fn, ref_kernels, ref_sampling) for name, fn in _s.SAMPLERS.items()})
 
 
 def uninstall() -> None:

@@ -15,6 +15,12 @@ def _is_pow2(x: int) -> bool:
     return x > 0 and (x & (x - 1)) == 0
 
 
+class OutOfBoundsError(IndexError):
+    """A lane addressed outside a global array (warp.py:33-34, raised by
+    GlobalArray2D._check, warp.py:234-240).  The device path raises it once,
+    before any launch, for word ids outside [0, V) of phi."""
+
+
 @dataclass(frozen=True)
 class WarpConfig:
     lanes: int = 32  # W, power of 2

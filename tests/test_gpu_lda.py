@@ -247,3 +247,77 @@ def test_theta_resample_wide_k_moments_and_long_document():
     # the long document: Dir(alpha + 300 * counts) concentrates near its mean
     a2 = alpha + 300 * counts
     assert np.abs(th[M] - a2 / a2.sum()).max() < 0.02
+
+
+def test_device_chain_matches_reference_chain_at_cfg3_scale():
+    """North-star acceptance at scale: a cfg3-shaped corpus
+    (200k documents, N ~ Poisson(200), V = 40k, K = 200, uniform words), 10
+    iterations from the same start (the reference's init_assignments +
+    resample at iteration -1, lda.py:262-265).
+
+    * reference chain: parity mode (device draw, numpy Gammas; bit-identical
+      to warpdraw.run_gibbs, tests/test_gpu_parity.py);
+    * device chain: DeviceLDA (device Philox Gammas);
+    * calibration chain: the reference algorithm with a different numpy
+      resample seed (same draw stream).
+
+    Iteration 0 draws from identical parameters, so its z must be identical.
+    The log-likelihood of the device chain is within 1e-3 relative of the
+    reference chain's at every iteration.  Per-topic token totals after the
+    last iteration: the chi-square distance device-vs-reference is compared
+    with reference-vs-calibration (both are distances between two
+    independent chains of the same sampler from the same start; the chains'
+    own Dirichlet noise makes the totals overdispersed w.r.t. a multinomial,
+    ~8x in chi-square, so the plain chi-square against K - 1 dof is not the
+    null): ratio below the F(K-1, K-1) 0.999 quantile."""
+    from scipy.stats import f as f_dist
+
+    from paper_1505_03851_b200 import lda as L
+    from paper_1505_03851_b200.kernels import draw_z_device
+    from paper_1505_03851_b200.rng import derive_seed
+
+    M, V, K, seed, iters = 200_000, 40_000, 200, 11, 10
+    gen = np.random.default_rng(seed)
+    N = np.maximum(gen.poisson(200.0, size=M), 1).astype(np.int64)
+    flat = gen.integers(0, V, size=int(N.sum()))
+    off = np.concatenate([[0], np.cumsum(N)])
+    c = L.Corpus(vocab_size=V, lengths=N, words=[flat[off[m]:off[m + 1]] for m in range(M)]).padded(32)
+    z0 = L.init_assignments(c, K, seed)
+    p0 = L.resample_params(c, z0, K, 0.1, 0.01, seed, -1, dtype=np.float32)
+    dc = c.to_device()
+    dev = DeviceLDA(dc, K, V, seed=seed)
+    dev.theta.copy_(torch.from_numpy(p0.theta))
+    dev.phi.copy_(torch.from_numpy(p0.phi))
+    ll_eval = DeviceLDA(dc, K, V, seed=seed)  # device log-likelihood of host parameters
+
+    def ll_of(params):
+        ll_eval.theta.copy_(torch.from_numpy(params.theta))
+        ll_eval.phi.copy_(torch.from_numpy(params.phi))
+        return ll_eval.log_likelihood()
+
+    def host_chain_step(params, t, resample_seed):
+        z = draw_z_device("butterfly", dc, torch.from_numpy(params.theta).cuda(), torch.from_numpy(params.phi).cuda(),
+                          wd.SeededStops(derive_seed(seed, 1, t)))
+        dt, wt = L._device_counts(dc, z, K, V)
+        new = L._resample_from_counts(dt.cpu().numpy().astype(np.int64), wt.cpu().numpy().astype(np.int64), 0.1,
+                                      0.01, resample_seed, t, np.float32)
+        return new, z
+
+    ref, alt = p0, p0
+    for t in range(iters):
+        ref, z_ref = host_chain_step(ref, t, seed)
+        alt, z_alt = host_chain_step(alt, t, seed + 1000)
+        dev.iterate(t)
+        if t == 0:
+            assert torch.equal(z_ref, dev.z)
+        a, b = ll_of(ref), dev.log_likelihood()
+        assert abs(a - b) / abs(a) < 1e-3, (t, a, b)
+    dev.check_errors()
+    t_ref = torch.bincount(z_ref.long(), minlength=K).double().cpu().numpy()
+    t_dev = torch.bincount(dev.z.long(), minlength=K).double().cpu().numpy()
+    t_alt = torch.bincount(z_alt.long(), minlength=K).double().cpu().numpy()
+    chi_dev = np.sum((t_dev - t_ref) ** 2 / (t_dev + t_ref))
+    chi_alt = np.sum((t_alt - t_ref) ** 2 / (t_alt + t_ref))
+    crit = f_dist.ppf(0.999, K - 1, K - 1)
+    assert chi_dev / chi_alt < crit, (chi_dev, chi_alt, crit)
+    assert chi_alt / chi_dev < crit, (chi_dev, chi_alt, crit)

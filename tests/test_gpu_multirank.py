@@ -87,9 +87,12 @@ def test_bench_nccl_path_world1():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
            "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "1", "--force-dist", "--steps", "2",
-           "--warmup", "3", "--no-cpu", "--no-sampler", "--docs-per-gpu", "64000", "--vocab", "40000"]
+           "--warmup", "3", "--no-cpu", "--no-sampler", "--no-dropin", "--docs", "64000", "--vocab", "40000"]
     r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 1 and line["value"] > 0 and line["e2e"]["value"] > 0
-    assert line["config"]["vocab_tiles"] == 4
+    assert line["roofline"]["launches_per_draw"] == 4
+    assert line["roofline"]["bound"] == "l2" and 0 < line["roofline"]["frac"] <= 1.2
+    assert line["scaling"] == "strong" and line["tokens_per_step"] == line["tokens_rank0"]
+    assert "nranks 1" in r.stderr or "nRanks 1" in r.stderr  # NCCL communicator line (NCCL_DEBUG=INFO)

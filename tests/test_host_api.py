@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared_symbols():
     text = open(os.path.join(ROOT, "include", "warpdraw_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:const char\*|int|size_t)\s+(wd_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const char\*|int|int64_t|size_t)\s+(wd_\w+)\(", text, re.M)))
 
 
 def test_header_declares_the_bound_exports():
@@ -205,3 +205,37 @@ def test_philox_known_answers():
     ]
     for ctr, key, out in kat:
         assert [int(x) for x in philox4x32_10(ctr, key)] == out
+
+
+def test_host_helper_ragged_loops_match_numpy():
+    """csrc/wd_host.c (the boundary's ragged <-> CSR loops) against numpy."""
+    from paper_1505_03851_b200 import kernels as K
+
+    assert K._wdhost is not None, "host helper not built"
+    gen = np.random.default_rng(4)
+    N = gen.integers(0, 9, size=500)
+    for dt in (np.int64, np.int32, np.int16, np.uint16, np.uint8):
+        w = [gen.integers(0, 200, size=int(n) + int(gen.integers(0, 3))).astype(dt) for n in N]
+        off, flat = K.ragged_to_csr(N, w)
+        ref = np.concatenate([x[:n] for x, n in zip(w, N)]).astype(np.int32)
+        np.testing.assert_array_equal(flat, ref)
+        assert flat.dtype == np.int32 and off[-1] == N.sum()
+    with pytest.raises(ValueError, match="shorter"):
+        K.ragged_to_csr([3], [np.arange(2)])
+    with pytest.raises(wd.OutOfBoundsError):
+        K.ragged_to_csr([2], [np.array([1, 1 << 40])])
+    # non-ndarray elements take the numpy path
+    off, flat = K.ragged_to_csr([2, 1], [[1, 2], (7,)])
+    np.testing.assert_array_equal(flat, [1, 2, 7])
+    z = np.arange(int(N.sum()), dtype=np.int64)
+    off = np.concatenate([[0], np.cumsum(N)])
+    views = K.csr_to_ragged(z, off)
+    assert len(views) == N.size and all(v.dtype == np.int64 for v in views)
+    for m in range(N.size):
+        np.testing.assert_array_equal(views[m], z[off[m]:off[m + 1]])
+    ids = K._wdhost.list_ids(views)
+    assert K._wdhost.ids_equal(views, ids)
+    views2 = list(views)
+    views2[7] = views2[7].copy()
+    assert not K._wdhost.ids_equal(views2, ids)
+    assert not K._wdhost.ids_equal(views[:-1], ids)

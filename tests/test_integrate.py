@@ -1,19 +1,30 @@
-"""The install() shim patches the reference package in place (CPU-side check;
-the reference is only importable in the build container, so this skips on
-the GPU box).  With a GPU, the patched reference's own run_gibbs must
-reproduce its unpatched golden output."""
+"""The install() shim patches the reference package in place (CPU-side
+checks).  The reference is importable from /root/reference in the build
+container and from baseline/_ref (the unmodified reference, pip-installed
+there; git-ignored, it travels to the GPU box) everywhere else; the GPU run
+of the patched reference's own run_gibbs is tests/test_gpu_reference_api.py."""
 
 import os
 import sys
 
 import pytest
 
-REF = os.environ.get("WARPDRAW_REF", "/root/reference/pkg/src")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def reference_path():
+    for cand in (os.environ.get("WARPDRAW_REF"), os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if cand and os.path.isdir(os.path.join(cand, "warpdraw")):
+            return cand
+    return None
+
+
+REF = reference_path()
 
 
 @pytest.fixture
 def warpdraw():
-    if not os.path.isdir(REF):
+    if REF is None:
         pytest.skip("reference package not present")
     sys.path.insert(0, REF)
     try:
@@ -59,3 +70,20 @@ def test_reference_stops_objects_are_recognised(warpdraw):
     assert isinstance(j, kernels.InjectedStops)
     assert [list(u) for u in j._units] == [[0.25, 0.5], [], [0.75]]
     assert integrate._convert(3, warpdraw.kernels) == 3
+
+
+def test_sampler_errors_are_the_reference_classes(warpdraw):
+    """SAMPLERS installed into warpdraw.bench raise the reference's own
+    exception classes (the weight validation runs before any device work)."""
+    import numpy as np
+
+    from paper_1505_03851_b200 import integrate
+
+    integrate.install()
+    try:
+        with pytest.raises(warpdraw.sampling.AllZeroError):
+            warpdraw.bench.SAMPLERS["alias"](np.zeros(4), 3, 1)
+        with pytest.raises(warpdraw.sampling.EmptyWeightsError):
+            warpdraw.bench.SAMPLERS["alias"](np.zeros(0), 3, 1)
+    finally:
+        integrate.uninstall()

@@ -132,3 +132,50 @@ def test_two_rank_gloo_tile_allreduce(tmp_path):
     total = sum(np.load(tmp_path / f"tiles_local{r}.npy") for r in range(world))
     for r in range(world):
         np.testing.assert_array_equal(np.load(tmp_path / f"tiles_wt{r}.npy"), total)
+
+
+def _bench_args(scaling):
+    import argparse
+
+    return argparse.Namespace(seed=5, docs=1000, mean_len=20.0, vocab=300, scaling=scaling)
+
+
+def _strong_shard_worker(rank, world, port, out_dir):
+    """bench.make_shard under --scaling strong: every rank generates the same
+    corpus and keeps its shard_ranges slice; the gathered shards must tile
+    the corpus exactly (documents, offsets, words, global doc ids)."""
+    import bench
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    off, words, doc_base = bench.make_shard(torch, rank, world, _bench_args("strong"), torch.device("cpu"))
+    meta = torch.tensor([doc_base, off.numel() - 1, words.numel()], dtype=torch.int64)
+    metas = [torch.zeros(3, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(metas, meta)
+    np.save(os.path.join(out_dir, f"off{rank}.npy"), off.numpy())
+    np.save(os.path.join(out_dir, f"words{rank}.npy"), words.numpy())
+    np.save(os.path.join(out_dir, f"meta{rank}.npy"), torch.stack(metas).numpy())
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_strong_shards_tile_the_corpus(tmp_path):
+    import bench
+
+    world = 2
+    mp.start_processes(_strong_shard_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    off1, words1, base1 = bench.make_shard(torch, 0, 1, _bench_args("strong"), torch.device("cpu"))
+    assert base1 == 0
+    metas = np.load(tmp_path / "meta0.npy")
+    np.testing.assert_array_equal(metas, np.load(tmp_path / "meta1.npy"))
+    assert metas[0, 0] == 0 and metas[1, 0] == metas[0, 1]  # contiguous, 32-aligned cuts
+    assert metas[1, 0] % 32 == 0 and metas[:, 1].sum() == off1.numel() - 1
+    words = np.concatenate([np.load(tmp_path / f"words{r}.npy") for r in range(world)])
+    np.testing.assert_array_equal(words, words1.numpy())
+    lens = np.concatenate([np.diff(np.load(tmp_path / f"off{r}.npy")) for r in range(world)])
+    np.testing.assert_array_equal(lens, np.diff(off1.numpy()))
+    tok = metas[:, 2]
+    assert abs(int(tok[0]) - int(tok[1])) < 0.05 * tok.sum()  # token-balanced
+    # weak scaling: rank r's corpus is its own (seed + r), doc_base = r x M
+    offw, _, basew = bench.make_shard(torch, 1, 2, _bench_args("weak"), torch.device("cpu"))
+    assert basew == offw.numel() - 1
