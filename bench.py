@@ -388,6 +388,8 @@ def l2_read_peak(torch, dev):
             if gbs > best:
                 best, best_cfg = gbs, (mb, blocks)
         del buf
+    if best_cfg is None:
+        raise RuntimeError("wd_l2_read_probe measured no bandwidth")
     return best, best_cfg
 
 
@@ -470,6 +472,11 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    # stdout carries exactly one JSON line: everything else written to fd 1
+    # (NCCL's INFO lines, library chatter) goes to stderr
+    sys.stdout.flush()
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     import torch
     import torch.distributed as dist
 
@@ -482,12 +489,14 @@ def main():
     if world > 1 or args.force_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
-        # communicator lines (nranks, NVLS / P2P transport) on stderr
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        # communicator lines (nranks, NVLS / P2P transport): NCCL prints them
+        # on its stdout, which points at stderr from here on (see json_out)
+        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+            os.environ["NCCL_DEBUG"] = "INFO"
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries only the JSON line
         dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
         pg = dist.group.WORLD
+        dist.barrier()  # the communicator exists (and has logged) before any timing
     K, V = args.topics, args.vocab
     hbm_peak, hbm_src = load_peaks()
 
@@ -708,7 +717,7 @@ def main():
             "sampler": sampler,
             "head": git_head(),
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=json_out, flush=True)
     if pg is not None:
         dist.destroy_process_group()
 

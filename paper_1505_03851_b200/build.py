@@ -30,6 +30,27 @@ STATISTICAL_SOURCES = {"wd_resample.cu"}
 
 
 HOST_SRC = os.path.join(CSRC, "wd_host.c")
+IO_SRC = os.path.join(CSRC, "wd_io.c")
+IO_LIB = os.path.join(OUT_DIR, "libwdio.so")
+
+
+def build_io(force: bool = False) -> str:
+    """libwdio.so: the native corpus / stop-file parsers and CSV writers
+    (csrc/wd_io.c, plain C over pthreads, loaded with ctypes by corpus_io)."""
+    if not force and os.path.exists(IO_LIB) and os.path.getmtime(IO_LIB) >= os.path.getmtime(IO_SRC):
+        return IO_LIB
+    cc = os.environ.get("CC") or shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        raise RuntimeError("no C compiler for libwdio")
+    os.makedirs(OUT_DIR, exist_ok=True)
+    tmp = IO_LIB + ".tmp"
+    # no fast-math: strtod / printf must stay correctly rounded
+    cmd = [cc, "-O2", "-shared", "-fPIC", "-std=c11", "-Wall", "-pthread", IO_SRC, "-o", tmp, "-lm"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"libwdio build failed:\n{r.stderr}")
+    os.replace(tmp, IO_LIB)
+    return IO_LIB
 
 
 def host_ext_path() -> str:
@@ -79,7 +100,7 @@ def _flags(ptxas_verbose: bool):
 
 
 def _deps():
-    return [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f != "wd_host.c"] + \
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f not in ("wd_host.c", "wd_io.c")] + \
         [os.path.join(INCLUDE, "warpdraw_b200.h")]
 
 
@@ -92,6 +113,7 @@ def up_to_date() -> bool:
 
 def build(force: bool = False, ptxas_verbose: bool = False, verbose: bool = True) -> str:
     build_host(force)
+    build_io(force)
     if not force and up_to_date():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)

@@ -5,7 +5,7 @@
 // not HBM.  This kernel measures that ceiling in the same process as the
 // draw: a grid-stride sweep of U independent 256-bit loads per thread
 // (ld.global.cg, L1 bypassed) over an L2-resident buffer, repeated `reps`
-// times.  Bytes read = the whole U * stride sweeps (wd_l2_probe_bytes).
+// times.  Bytes read per rep = the whole buffer (wd_l2_probe_bytes).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -23,15 +23,21 @@ __global__ void __launch_bounds__(kProbeThreads) l2_read_probe(const float* __re
   float acc = 0.f;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int r = 0; r < reps; ++r)
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i + (kProbeU - 1) * stride < n8;
-         i += kProbeU * stride) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += kProbeU * stride) {
+      // U independent loads in flight per thread; the tail of the last sweep
+      // is predicated off, so every 32-byte element is read once per rep
       float v[kProbeU][8];
 #pragma unroll
-      for (int u = 0; u < kProbeU; ++u)
-        asm volatile("ld.global.cg.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=f"(v[u][0]), "=f"(v[u][1]), "=f"(v[u][2]), "=f"(v[u][3]), "=f"(v[u][4]), "=f"(v[u][5]),
-                       "=f"(v[u][6]), "=f"(v[u][7])
-                     : "l"(p + 8 * (i + u * stride)));
+      for (int u = 0; u < kProbeU; ++u) {
+        const int64_t j = i + u * stride;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[u][e] = 0.f;
+        if (j < n8)
+          asm volatile("ld.global.cg.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=f"(v[u][0]), "=f"(v[u][1]), "=f"(v[u][2]), "=f"(v[u][3]), "=f"(v[u][4]), "=f"(v[u][5]),
+                         "=f"(v[u][6]), "=f"(v[u][7])
+                       : "l"(p + 8 * j));
+      }
 #pragma unroll
       for (int u = 0; u < kProbeU; ++u)
 #pragma unroll
@@ -45,8 +51,8 @@ __global__ void __launch_bounds__(kProbeThreads) l2_read_probe(const float* __re
 extern "C" {
 
 int64_t wd_l2_probe_bytes(int64_t buffer_bytes, int blocks) {
-  const int64_t n8 = buffer_bytes / 32, stride = (int64_t)blocks * wd::kProbeThreads;
-  return n8 >= wd::kProbeU * stride ? (n8 / (wd::kProbeU * stride)) * wd::kProbeU * stride * 32 : 0;
+  (void)blocks;  // every 32-byte element of the buffer is read once per rep, for any grid
+  return (buffer_bytes / 32) * 32;
 }
 
 int wd_l2_read_probe(const void* buffer, int64_t buffer_bytes, int reps, int blocks, float* sink, void* stream) {

@@ -78,6 +78,21 @@ class InjectedStops:
 
     def __init__(self, units):
         self._units = [np.asarray(u, dtype=np.float64) for u in units]
+        self._csr = None  # (lengths, flat) when built from one flat CSR-order array
+
+    @classmethod
+    def from_flat(cls, flat, lengths) -> "InjectedStops":
+        """u per token in CSR (document, word) order, e.g. one row of
+        corpus_io.load_injected_units; the flat array is kept as the device
+        layout (no per-document concatenation in flat())."""
+        flat = np.ascontiguousarray(flat, dtype=np.float64)
+        lengths = np.asarray(lengths, dtype=np.int64)
+        off = np.concatenate([[0], np.cumsum(lengths)])
+        if flat.size != int(off[-1]):
+            raise ValueError(f"{flat.size} values for {int(off[-1])} tokens")
+        st = cls(csr_to_ragged(flat, off))
+        st._csr = (lengths, flat)
+        return st
 
     @classmethod
     def from_seed(cls, seed: int, lengths) -> "InjectedStops":
@@ -87,15 +102,16 @@ class InjectedStops:
 
     @classmethod
     def from_file(cls, path, lengths) -> "InjectedStops":
-        flat = np.loadtxt(path, dtype=np.float64, ndmin=1)
+        from .corpus_io import read_floats  # np.loadtxt semantics, native parser
+
+        flat = read_floats(path)
         if flat.size != int(np.sum(lengths)):
             raise ValueError(
                 f"stop file {path} holds {flat.size} values, corpus needs {int(np.sum(lengths))}"
             )
         if np.any(flat < 0) or np.any(flat >= 1):
             raise ValueError("injected values must lie in [0, 1)")
-        off = np.concatenate([[0], np.cumsum(np.asarray(lengths, dtype=np.int64))])
-        return cls(csr_to_ragged(flat, off))
+        return cls.from_flat(flat, lengths)
 
     def units(self, m, i, i_master):
         mm = np.atleast_1d(np.asarray(m))
@@ -109,6 +125,8 @@ class InjectedStops:
     def flat(self, lengths) -> np.ndarray:
         """u in CSR token order (doc-major), the device layout."""
         lengths = np.asarray(lengths, dtype=np.int64)
+        if self._csr is not None and np.array_equal(self._csr[0], lengths):
+            return self._csr[1]
         if len(self._units) == lengths.size:
             lens = np.fromiter(map(len, self._units), dtype=np.int64, count=lengths.size)
             if np.array_equal(lens, lengths):
