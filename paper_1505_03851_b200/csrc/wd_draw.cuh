@@ -96,6 +96,7 @@ template <typename T> struct DrawParams {
   int l2_policy_x;          // L2 policy of the phi / weights loads (see make_l2_policy)
   int l2_policy_t;          // L2 policy of the theta loads
   uint32_t opaque_zero;     // always 0; the compiler cannot prove it (see BlockRegs::join)
+  int theta_prefetch;       // lean LDA draw: L2 prefetch distance (blocks) of the theta segments, 0 = off
 };
 
 // Identity of the token/row a lane owns: global doc id (or row id), its hash

@@ -12,6 +12,7 @@
 #include <utility>
 
 #include "wd_draw.cuh"
+#include "wd_lean.cuh"
 #include "wd_shared.cuh"
 
 namespace wd {
@@ -244,6 +245,48 @@ int launch_rows_stash(const DrawParams<T>& p0, cudaStream_t st) {
   return WD_OK;
 }
 
+// The register-lean LDA draw (wd_lean.cuh): fp32, W = 32, 256-bit segments,
+// K % 32 == 0 with at least WD_LEAN_MIN_NB blocks.  WD_LEAN=0 disables it
+// (A/B against bfly_kernel).  Measured (tools/configs.py, draw ms, old ->
+// lean): K = 2048 145.2 -> 118.9, configs[4] shard (K = 4096) 363.6 -> 304.4;
+// at K = 1024 the general kernel is already at the L2 -> SM read ceiling
+// (ncu: 17.96 TB/s xbar -> L1) and lean is 1-2% slower, so it starts at 64
+// blocks.
+inline bool lean_eligible(const DrawParams<float>& p) {
+  static int on = env_int("WD_LEAN", 1);
+  static int min_nb = env_int("WD_LEAN_MIN_NB", 64);
+  return on && p.K % 32 == 0 && p.K / 32 >= min_nb;
+}
+inline int launch_lean(const DrawParams<float>& p0, cudaStream_t st) {
+  DrawParams<float> p = p0;
+  // theta streams from HBM once per vocabulary tile (evict_first) while the
+  // tile's phi slice should stay in L2 (evict_last): cfg5 shard 318 -> 304 ms
+  static int lx = env_int("WD_L2_X", 1), lt = env_int("WD_L2_T", 2);
+  p.l2_policy_x = lx;
+  p.l2_policy_t = lt;
+  static int pf = env_int("WD_LEAN_PF", 0);
+  // the warp-cooperative pass 2 moved fewer L1 wavefronts but measured
+  // slower (cfg5 shard 318 vs 335 ms, K = 2048 123 vs 127): off by default
+  static int coop = env_int("WD_LEAN_COOP", 0);
+  p.theta_prefetch = pf;
+  const void* fn = coop ? (const void*)lda_lean_kernel<WD_LEAN_MIN_BLOCKS, true>
+                        : (const void*)lda_lean_kernel<WD_LEAN_MIN_BLOCKS, false>;
+  const int wpb = kThreads / 32;
+  const size_t smem = (size_t)wpb * kLeanWarpFloats * sizeof(float);
+  const int per_sm = occupancy_blocks(fn, smem, kThreads);
+  if (per_sm <= 0) return WD_ERR_CUDA;
+  const int64_t chunks = (p.n_tokens + 31) / 32;
+  const int64_t want = (chunks + wpb - 1) / wpb;
+  const int64_t cap = (int64_t)per_sm * device_sm_count();
+  const int grid = (int)(want < cap ? want : cap);
+  if (grid <= 0) return WD_OK;
+  if (coop) lda_lean_kernel<WD_LEAN_MIN_BLOCKS, true><<<grid, kThreads, smem, st>>>(p);
+  else lda_lean_kernel<WD_LEAN_MIN_BLOCKS, false><<<grid, kThreads, smem, st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { set_last_cuda_error(e); return WD_ERR_CUDA; }
+  return WD_OK;
+}
+
 // Dispatch on (variant, W, VEC, MODE); explicit instantiations live in
 // wd_draw_f32.cu / wd_draw_f64.cu so the two element types compile in parallel.
 template <typename T>
@@ -258,6 +301,7 @@ int launch_draw(int variant, int W, int vec, int mode, const DrawParams<T>& p, v
     if (mode == MODE_LDA) {
       if constexpr (std::is_same<T, float>::value) {
         // 256-bit lane segments (vec 2: 32-byte aligned fp32 blocks, W = 32)
+        if (vec == 2 && W == 32 && lean_eligible(p)) return launch_lean(p, st);
         if (vec == 2 && W == 32) return launch_bfly_inst<T, 32, 2, MODE_LDA>(p, st);
       }
       return vec ? launch_bfly_w<T, true, MODE_LDA>(W, p, st) : launch_bfly_w<T, false, MODE_LDA>(W, p, st);

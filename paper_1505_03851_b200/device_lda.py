@@ -29,6 +29,17 @@ from .sharding import TileAllReduce, count_chunks
 # phi slice kept L2-resident per draw pass (126 MB L2; measured: 41 MB slices
 # run at the L2-resident rate, 82 MB ones do not -- profiles/)
 DEFAULT_VOCAB_TILE_BYTES = 40 << 20
+def lean_draw(K: int, lanes: int, elem_size: int) -> bool:
+    """True when the C ABI dispatches the draw to lda_lean_kernel (fp32,
+    W = 32, K a multiple of 32 with >= WD_LEAN_MIN_NB blocks, aligned rows;
+    csrc/wd_launch.cuh lean_eligible)."""
+    import os
+
+    if os.environ.get("WD_LEAN", "1") == "0":
+        return False
+    return elem_size == 4 and lanes == 32 and K % 32 == 0 and K // 32 >= int(os.environ.get("WD_LEAN_MIN_NB", "64"))
+
+
 # mean tokens per (document, tile) run from which runs are padded to the
 # butterfly kernel's lane-group height (VocabTiles.run_pad)
 RUN_PAD_MIN_MEAN_RUN = 20  # measured at K=1024 (runs ~50 tokens): draw -10%
@@ -85,6 +96,10 @@ class DeviceLDA:
                 # padding to 4 vs 8 -1.2%, Zipf -2.2%)
                 group = 4 if (self.lanes == 32 and esz == 4) else self.lanes // 4
                 run_pad = group if (self.lanes >= 8 and fine and mean_run >= RUN_PAD_MIN_MEAN_RUN) else 0
+                if lean_draw(self.K, self.lanes, esz):
+                    # the register-lean kernel (csrc/wd_lean.cuh) keeps one
+                    # theta segment per lane: runs padded to its 4-row groups
+                    run_pad = 4
             self.tiles = corpus.vocab_tiles(rows, run_pad)
         self._reducer = None  # in-flight per-tile count all-reduces (draw -> resample)
         n_err = self.tiles.n_tiles if self.tiles is not None else 1
