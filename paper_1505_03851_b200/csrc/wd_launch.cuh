@@ -13,6 +13,7 @@
 
 #include "wd_draw.cuh"
 #include "wd_lean.cuh"
+#include "wd_rows_lane.cuh"
 #include "wd_shared.cuh"
 
 namespace wd {
@@ -287,6 +288,57 @@ inline int launch_lean(const DrawParams<float>& p0, cudaStream_t st) {
   return WD_OK;
 }
 
+// Standalone rows with K = 8 * RM + 32 * NB, NB <= 4 (fp32, W = 32, 32-byte
+// aligned rows): one row per thread (wd_rows_lane.cuh).  WD_ROWS_LANE=0
+// disables it; WD_ROWS_LANE_MAX_NB caps the block count it takes.
+template <int NB, int RM>
+int launch_rows_lane_inst(const DrawParams<float>& p, cudaStream_t st) {
+  const void* fn = (const void*)rows_lane_kernel<NB, RM>;
+  const int per_sm = occupancy_blocks(fn, 0, kThreads);
+  if (per_sm <= 0) return WD_ERR_CUDA;
+  const int64_t want = (p.n_tokens + kThreads - 1) / kThreads;
+  const int64_t cap = (int64_t)per_sm * device_sm_count();
+  const int grid = (int)(want < cap ? want : cap);
+  if (grid <= 0) return WD_OK;
+  rows_lane_kernel<NB, RM><<<grid, kThreads, 0, st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { set_last_cuda_error(e); return WD_ERR_CUDA; }
+  return WD_OK;
+}
+template <int NB>
+int launch_rows_lane_nb(int rm, const DrawParams<float>& p, cudaStream_t st) {
+  switch (rm) {
+    case 0: if constexpr (NB > 0) return launch_rows_lane_inst<NB, 0>(p, st); else return WD_ERR_UNSUPPORTED;
+    case 1: return launch_rows_lane_inst<NB, 1>(p, st);
+    case 2: return launch_rows_lane_inst<NB, 2>(p, st);
+    case 3: return launch_rows_lane_inst<NB, 3>(p, st);
+    default: return WD_ERR_UNSUPPORTED;
+  }
+}
+// Measured against the warp-cooperative kernels (tools/sweep.py, 2^20 rows;
+// 2^24-row steady state in brackets, fraction of HBM): K = 8 / 16 / 24
+// 0.25 / 0.36 / 0.39 -> 0.40 / 0.52 / 0.60 (0.37 / 0.52 / 0.58 -> 0.90 /
+// 1.02 / 1.02); K = 40-56 and 136-152 (a remnant next to 1 or 4 blocks)
+// +5-11%; K = 32, 64-128 (whole blocks, 2-3 blocks) are as fast or faster
+// on the cooperative kernels (K = 64: 0.72 vs 0.58), which keep them.
+inline bool rows_lane_eligible(const DrawParams<float>& p) {
+  static int on = env_int("WD_ROWS_LANE", 1);  // 2: every shape it supports (A/B)
+  const int nb = p.K / 32, rm = (p.K % 32) / 8;
+  if (!on || p.ld_phi == 0 || (p.K % 32) % 8 != 0 || nb > 4) return false;
+  return on == 2 || nb == 0 || (rm > 0 && (nb == 1 || nb == 4));
+}
+inline int launch_rows_lane(const DrawParams<float>& p, cudaStream_t st) {
+  const int nb = p.K / 32, rm = (p.K % 32) / 8;
+  switch (nb) {
+    case 0: return launch_rows_lane_nb<0>(rm, p, st);
+    case 1: return launch_rows_lane_nb<1>(rm, p, st);
+    case 2: return launch_rows_lane_nb<2>(rm, p, st);
+    case 3: return launch_rows_lane_nb<3>(rm, p, st);
+    case 4: return launch_rows_lane_nb<4>(rm, p, st);
+    default: return WD_ERR_UNSUPPORTED;
+  }
+}
+
 // Dispatch on (variant, W, VEC, MODE); explicit instantiations live in
 // wd_draw_f32.cu / wd_draw_f64.cu so the two element types compile in parallel.
 template <typename T>
@@ -313,6 +365,8 @@ int launch_draw(int variant, int W, int vec, int mode, const DrawParams<T>& p, v
       // K = 32: the double-buffered own-row variant (rows_stash2_kernel,
       // measured 26.5 -> 31.1 G draws/s; at K = 64, two blocks per stage,
       // 20.4 -> 19.5: not used)
+      // one row per thread at small K (256-bit aligned rows)
+      if (vec == 2 && W == 32 && rows_lane_eligible(p)) return launch_rows_lane(p, st);
       if (vec && W == 32 && p.K == 32) {
         if (WD_STASH2 & 1) return launch_rows_stash<T, 32, 1, 2>(p, st);
         return launch_rows_stash<T, 32, 1>(p, st);
