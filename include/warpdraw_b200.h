@@ -227,6 +227,30 @@ int wd_stream_draws(int method, const double* table, const uint64_t* thresh, con
 int64_t wd_l2_probe_bytes(int64_t buffer_bytes, int blocks);
 int wd_l2_read_probe(const void* buffer, int64_t buffer_bytes, int reps, int blocks, float* sink, void* stream);
 
+/*
+ * The reference's split table / search API (the draw entry points fuse the
+ * two; these materialise the table exactly as the reference stores it).
+ *
+ * wd_build_block_tables replaces build_block_tables (kernels.py:580-600 ->
+ * build_butterfly_table, kernels.py:170-225): products [G][W][K] (each of
+ * the G warp groups holds W lanes' product rows; theta_local := products,
+ * phi := 1) -> p [K][G][W] (the butterfly-patterned table: lane-own
+ * remnant running sums, then per W-topic block the rows stored by the
+ * log2(W) shuffle_xor sets and the running total in row W-1) and
+ * sums [G][W].
+ *
+ * wd_butterfly_search replaces butterfly_search (kernels.py:317-362) with
+ * _butterfly_block_walk (kernels.py:268-314): block bisection over each
+ * lane's block-final rows, the cross-lane fetch walk, the remnant fallback;
+ * out [G][W] int64 indices.  err[2] as in wd_draw_z: err[1] == 0 when a
+ * stop lies outside [0, sums) (StopOutOfRangeError, kernels.py:329-331).
+ * lanes: 2..64.  dtype: WD_FLOAT32 / WD_FLOAT64.  Device pointers.
+ */
+int wd_build_block_tables(int dtype, int lanes, const void* products, int32_t n_topics, int64_t n_groups, void* p,
+                          void* sums, void* stream);
+int wd_butterfly_search(int dtype, int lanes, const void* p, const void* sums, const void* stops, int32_t n_topics,
+                        int64_t n_groups, int64_t* out, uint64_t* err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

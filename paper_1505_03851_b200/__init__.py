@@ -50,6 +50,7 @@ from .samplers import (
     sample_rows,
 )
 from .sampling import AllZeroError, EmptyWeightsError
+from .tables import ButterflyTable, build_block_tables, butterfly_search, table_snapshot
 from .warp import OutOfBoundsError, Trace, WarpConfig
 
 __version__ = "0.1.0"

@@ -43,6 +43,8 @@ EXPORTS = (
     "wd_stream_draws",
     "wd_l2_probe_bytes",
     "wd_l2_read_probe",
+    "wd_build_block_tables",
+    "wd_butterfly_search",
 )
 
 
@@ -97,6 +99,10 @@ def _declare(L):
     L.wd_l2_probe_bytes.argtypes = [i64, i32]
     L.wd_l2_read_probe.restype = i32
     L.wd_l2_read_probe.argtypes = [vp, i64, i32, i32, vp, vp]
+    L.wd_build_block_tables.restype = i32
+    L.wd_build_block_tables.argtypes = [i32, i32, vp, ctypes.c_int32, i64, vp, vp, vp]
+    L.wd_butterfly_search.restype = i32
+    L.wd_butterfly_search.argtypes = [i32, i32, vp, vp, vp, ctypes.c_int32, i64, vp, vp, vp]
 
 
 def load(path: str | None = None):

@@ -15,6 +15,9 @@ After install():
 * warpdraw.bench.SAMPLERS["binary" | "alias" | "butterfly"] are the GPU
   samplers (bench.py:150-154), bit-identical, and SAMPLERS["prefix"] (the
   butterfly's u stream through a full prefix table) is added;
+* warpdraw.kernels.build_block_tables / butterfly_search / table_snapshot
+  (and the names warpdraw.bench and warpdraw.cli imported from it) build and
+  search the butterfly table on the GPU (kernels.py:580-604, 317-362);
 * the reference's exception classes are the ones raised (AllZeroError,
   EmptyWeightsError, StopOutOfRangeError, OutOfBoundsError are mapped, for draw_z and SAMPLERS), and its SeededStops / InjectedStops
   objects are recognised (in-kernel hash / u per token).
@@ -28,6 +31,7 @@ import importlib
 
 from . import kernels as _k
 from . import samplers as _s
+from . import tables as _t
 from . import warp as _w
 
 _saved: dict = {}
@@ -82,6 +86,16 @@ def install(package: str = "warpdraw") -> None:
     ref_kernels.draw_z = gpu_draw_z
     ref_lda.draw_z = gpu_draw_z
     ref_bench.SAMPLERS.update({name: _wrap_errors(fn, ref_kernels, ref_sampling) for name, fn in _s.SAMPLERS.items()})
+    # the split table / search API: the defining module and the modules that
+    # imported the names (bench.py:19, cli.py uses kernels.<name>)
+    tabs = {"build_block_tables": _t.build_block_tables, "butterfly_search": _t.butterfly_search,
+            "table_snapshot": _t.table_snapshot}
+    _saved["tables"] = []
+    for mod in (ref_kernels, ref_bench):
+        for name, fn in tabs.items():
+            if hasattr(mod, name):
+                _saved["tables"].append((mod, name, getattr(mod, name)))
+                setattr(mod, name, _wrap_errors(fn, ref_kernels, ref_sampling))
 
 
 def uninstall() -> None:
@@ -96,3 +110,5 @@ def uninstall() -> None:
     ref_bench, samplers = _saved.pop("bench")
     ref_bench.SAMPLERS.clear()
     ref_bench.SAMPLERS.update(samplers)
+    for mod, name, fn in _saved.pop("tables", []):
+        setattr(mod, name, fn)

@@ -43,8 +43,16 @@ def test_install_patches_and_restores(warpdraw):
 
     orig_draw = warpdraw.kernels.draw_z
     orig_kernels = dict(warpdraw.kernels.KERNELS)
+    orig_tables = (warpdraw.kernels.build_block_tables, warpdraw.kernels.butterfly_search,
+                   warpdraw.bench.build_block_tables, warpdraw.bench.butterfly_search)
     integrate.install()
     try:
+        # the split table / search API (kernels.py:580-604, 317-362) and
+        # bench.py's imported names (bench.py:19)
+        assert warpdraw.kernels.build_block_tables is not orig_tables[0]
+        assert warpdraw.kernels.butterfly_search is not orig_tables[1]
+        assert warpdraw.bench.build_block_tables is not orig_tables[2]
+        assert warpdraw.bench.butterfly_search is not orig_tables[3]
         assert warpdraw.kernels.draw_z is not orig_draw
         assert warpdraw.lda.draw_z is warpdraw.kernels.draw_z
         assert set(warpdraw.kernels.KERNELS) == {"basic", "transposed", "butterfly"}
@@ -57,6 +65,8 @@ def test_install_patches_and_restores(warpdraw):
         integrate.uninstall()
     assert warpdraw.kernels.draw_z is orig_draw
     assert warpdraw.kernels.KERNELS == orig_kernels
+    assert (warpdraw.kernels.build_block_tables, warpdraw.kernels.butterfly_search, warpdraw.bench.build_block_tables,
+            warpdraw.bench.butterfly_search) == orig_tables
     assert "prefix" not in warpdraw.bench.SAMPLERS
 
 
