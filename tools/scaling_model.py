@@ -1,0 +1,113 @@
+"""Strong-scaling model of configs[3] (the bench corpus, K = 1024) on 2/4/8 GPUs,
+measured one shard at a time on ONE GPU (the only hardware this round has).
+
+For N in 1, 2, 4, 8 the 1M-document corpus is cut exactly as `bench.py
+--gpus N` cuts it (sharding.shard_ranges: 32-aligned, token-balanced) and
+the first and last rank's shards are run alone through DeviceLDA (no process
+group): draw, theta resample and phi resample timed separately with CUDA
+events.  A rank's iteration at N GPUs is then
+
+    T_N = draw_N + theta_N + phi + allreduce_tail_N
+
+where phi (V x K, every rank resamples it identically) does not shrink with
+N, and the count all-reduce is hidden behind the next vocabulary tile's draw
+except the LAST tile's rows (DeviceLDA draw(overlap_allreduce=True)), whose
+all-reduce is exposed: bytes = (V / tiles) x K x 4, time = 2 (N-1)/N x bytes
+/ busbw (ring all-reduce), busbw an assumption given on the command line
+(default 700 GB/s: NCCL all-reduce bus bandwidth on 8 x B200 NVLink 5; NVLS
+in-switch reduction would only lower it).  Predicted strong-scaling
+efficiency = T_1 / (N * max(T_N over ranks)).  Prints one JSON object.
+
+    python tools/scaling_model.py [--busbw-gbs 700] [--steps 5]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+import paper_1505_03851_b200 as wd  # noqa: E402
+from paper_1505_03851_b200 import _lib  # noqa: E402
+from paper_1505_03851_b200.device_lda import DeviceLDA  # noqa: E402
+from paper_1505_03851_b200.rng import derive_seed  # noqa: E402
+
+
+def time_shard(args, rank, world, dev):
+    a = argparse.Namespace(**vars(args))
+    a.scaling = "strong"
+    off, words, doc_base = bench.make_shard(torch, rank, world, a, dev)
+    dc = wd.DeviceCorpus.from_csr(off, words, doc_base=doc_base, vocab_size=a.vocab)
+    del words
+    lda = DeviceLDA(dc, a.topics, a.vocab, lanes=32, seed=a.seed)
+    lda.init_uniform()
+    for t in range(2):
+        lda.iterate(t)
+    torch.cuda.synchronize()
+    L = _lib.load()
+    st = torch.cuda.current_stream()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    for s in range(args.steps):
+        t = 10 + s
+        e = ev[s]
+        e[0].record(st)
+        lda.draw(t)
+        e[1].record(st)
+        _lib.check(L.wd_resample_theta(lda._dt, lda.z.data_ptr(), dc.offsets.data_ptr(), dc.n_docs, lda.K, lda.alpha,
+                                       derive_seed(lda.seed, 2, t, 0), dc.doc_base, lda.theta.data_ptr(),
+                                       lda.theta.stride(0), _lib.stream_handle()), "theta")
+        e[2].record(st)
+        _lib.check(L.wd_resample_phi(lda._dt, lda.word_topic.data_ptr(), lda.V, lda.K, lda.beta,
+                                     derive_seed(lda.seed, 2, t, 1), lda.phi.data_ptr(), lda.phi.stride(0),
+                                     lda._phi_ws.data_ptr(), lda._phi_ws.numel(), _lib.stream_handle()), "phi")
+        e[3].record(st)
+    torch.cuda.synchronize()
+    mean = lambda i, j: sum(x[i].elapsed_time(x[j]) for x in ev) / len(ev)  # noqa: E731
+    out = {"rank": rank, "docs": dc.n_docs, "tokens": dc.n_tokens, "draw_ms": mean(0, 1), "theta_ms": mean(1, 2),
+           "phi_ms": mean(2, 3), "iter_ms": mean(0, 3), "vocab_tiles": lda.tiles.n_tiles,
+           "rows_per_tile": lda.tiles.rows_per_tile}
+    del lda, dc
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--busbw-gbs", type=float, default=700.0)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--docs", type=int, default=1_000_000)
+    ap.add_argument("--topics", type=int, default=1024)
+    ap.add_argument("--vocab", type=int, default=40_000)
+    ap.add_argument("--mean-len", type=float, default=200.0)
+    ap.add_argument("--seed", type=int, default=2026)
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    res = {"assumption": f"ring all-reduce busbw {args.busbw_gbs} GB/s (NVLink 5); only the last vocabulary tile's "
+                         "count all-reduce is exposed", "per_n": {}}
+    t1 = None
+    for N in (1, 2, 4, 8):
+        ranks = sorted({0, N - 1})
+        shards = [time_shard(args, r, N, dev) for r in ranks]
+        worst = max(shards, key=lambda s: s["iter_ms"])
+        tile_bytes = worst["rows_per_tile"] * args.topics * 4
+        ar_ms = 0.0 if N == 1 else 2 * (N - 1) / N * tile_bytes / (args.busbw_gbs * 1e9) * 1e3
+        t_n = worst["iter_ms"] + ar_ms
+        if N == 1:
+            t1 = t_n
+        if N == 1:
+            total_tokens = shards[0]["tokens"]
+        res["per_n"][N] = {"shards": shards, "exposed_allreduce_ms": ar_ms, "predicted_iter_ms": t_n,
+                           "predicted_tokens_per_s": total_tokens / (t_n / 1e3),
+                           "predicted_efficiency": t1 / (N * t_n)}
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
