@@ -14,6 +14,7 @@
 #include "wd_draw.cuh"
 #include "wd_lean.cuh"
 #include "wd_rows_lane.cuh"
+#include "wd_small.cuh"
 #include "wd_shared.cuh"
 
 namespace wd {
@@ -339,6 +340,58 @@ inline int launch_rows_lane(const DrawParams<float>& p, cudaStream_t st) {
   }
 }
 
+// The small-K LDA draw (wd_small.cuh): K = 8 * RM + 32 * NB, 2 <= NB <= 8,
+// fp32, W = 32, 256-bit aligned rows.  WD_SMALL_LDA: 0 off, 1 on vocabulary
+// tiles (DeviceLDA's run-padded token order), 2 also on CSR-order draws.
+template <int NB, int RM>
+int launch_small_inst(const DrawParams<float>& p, cudaStream_t st) {
+  const void* fn = (const void*)lda_small_kernel<NB, RM>;
+  const int wpb = kThreads / 32;
+  const size_t smem = (size_t)wpb * NB * 4 * 40 * sizeof(float);
+  const int per_sm = occupancy_blocks(fn, smem, kThreads);
+  if (per_sm <= 0) return WD_ERR_CUDA;
+  const int64_t chunks = (p.n_tokens + 31) / 32;
+  const int64_t want = (chunks + wpb - 1) / wpb;
+  const int64_t cap = (int64_t)per_sm * device_sm_count();
+  const int grid = (int)(want < cap ? want : cap);
+  if (grid <= 0) return WD_OK;
+  lda_small_kernel<NB, RM><<<grid, kThreads, smem, st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { set_last_cuda_error(e); return WD_ERR_CUDA; }
+  return WD_OK;
+}
+template <int NB>
+int launch_small_nb(int rm, const DrawParams<float>& p, cudaStream_t st) {
+  switch (rm) {
+    case 0: return launch_small_inst<NB, 0>(p, st);
+    case 1: return launch_small_inst<NB, 1>(p, st);
+    case 2: return launch_small_inst<NB, 2>(p, st);
+    case 3: return launch_small_inst<NB, 3>(p, st);
+    default: return WD_ERR_UNSUPPORTED;
+  }
+}
+inline bool small_lda_eligible(const DrawParams<float>& p) {
+  static int on = env_int("WD_SMALL_LDA", 1);
+  const int nb = p.K / 32;
+  if (!on || (p.K % 32) % 8 != 0 || nb < 2 || nb > 8) return false;
+  return on == 2 || p.token_pos != nullptr;
+}
+inline int launch_small_lda(const DrawParams<float>& p0, cudaStream_t st) {
+  DrawParams<float> p = p0;
+  l2_policies(MODE_LDA, p.l2_policy_x, p.l2_policy_t);
+  const int rm = (p.K % 32) / 8;
+  switch (p.K / 32) {
+    case 2: return launch_small_nb<2>(rm, p, st);
+    case 3: return launch_small_nb<3>(rm, p, st);
+    case 4: return launch_small_nb<4>(rm, p, st);
+    case 5: return launch_small_nb<5>(rm, p, st);
+    case 6: return launch_small_nb<6>(rm, p, st);
+    case 7: return launch_small_nb<7>(rm, p, st);
+    case 8: return launch_small_nb<8>(rm, p, st);
+    default: return WD_ERR_UNSUPPORTED;
+  }
+}
+
 // Dispatch on (variant, W, VEC, MODE); explicit instantiations live in
 // wd_draw_f32.cu / wd_draw_f64.cu so the two element types compile in parallel.
 template <typename T>
@@ -354,6 +407,7 @@ int launch_draw(int variant, int W, int vec, int mode, const DrawParams<T>& p, v
       if constexpr (std::is_same<T, float>::value) {
         // 256-bit lane segments (vec 2: 32-byte aligned fp32 blocks, W = 32)
         if (vec == 2 && W == 32 && lean_eligible(p)) return launch_lean(p, st);
+        if (vec == 2 && W == 32 && small_lda_eligible(p)) return launch_small_lda(p, st);
         if (vec == 2 && W == 32) return launch_bfly_inst<T, 32, 2, MODE_LDA>(p, st);
       }
       return vec ? launch_bfly_w<T, true, MODE_LDA>(W, p, st) : launch_bfly_w<T, false, MODE_LDA>(W, p, st);
