@@ -5,7 +5,8 @@ The launchers read their knobs once per process (csrc/wd_launch.cuh), so each
 setting runs in a child process: the register-lean LDA draw
 (WD_LEAN_MIN_NB=16 takes it down to K = 512, WD_LEAN_COOP=1 its warp-
 cooperative pass 2, WD_LEAN_PF its theta L2 prefetch), the one-row-per-thread
-rows kernel on every shape it supports (WD_ROWS_LANE=2), and both disabled
+rows kernel on every shape it supports (WD_ROWS_LANE=2), the small-K LDA
+kernel on CSR-order draws too (WD_SMALL_LDA=2), and all of them disabled
 (the general kernels on the same shapes)."""
 
 import json
@@ -40,7 +41,7 @@ for K in (8, 16, 24, 32, 40, 56, 64, 72, 104, 128, 136, 152):
     got = wd.sample_rows(torch.from_numpy(w).cuda(), seed, lanes=32, check=False).cpu().numpy()
     exp = O.sample_rows(w, 32, wd.derive_seed(seed, 6), threads=8)
     out["rows"].append([K, int(np.sum(got != exp))])
-for K in (512, 1024, 2048):
+for K in (72, 200, 256, 512, 1024, 2048):
     for pad in (0, 4):
         gen = np.random.default_rng(K + pad)
         M, V = 512, 400
@@ -64,7 +65,8 @@ SETTINGS = {
     "lean_k512": {"WD_LEAN_MIN_NB": "16"},
     "lean_coop_pf": {"WD_LEAN_MIN_NB": "16", "WD_LEAN_COOP": "1", "WD_LEAN_PF": "3"},
     "rows_lane_all": {"WD_ROWS_LANE": "2"},
-    "general_only": {"WD_LEAN": "0", "WD_ROWS_LANE": "0"},
+    "small_lda_all": {"WD_SMALL_LDA": "2"},
+    "general_only": {"WD_LEAN": "0", "WD_ROWS_LANE": "0", "WD_SMALL_LDA": "0"},
 }
 
 
