@@ -183,6 +183,24 @@ size_t wd_resample_phi_workspace_bytes(int32_t n_topics);
 int wd_resample_phi(int dtype, const int32_t* word_topic, int64_t vocab_size, int32_t n_topics,
                     double beta, uint64_t seed, void* phi, int64_t ld_phi, void* workspace,
                     size_t workspace_bytes, void* stream);
+/*
+ * The same phi resample split for a document-sharded multi-GPU run (the
+ * ranks hold identical all-reduced counts): the V rows are cut into
+ * wd_resample_phi_chunks() fixed chunks; pass p (0: Gammas + column maxima,
+ * 1: exp + column sums, 2: normalise) runs chunks [chunk0, chunk1) and writes
+ * their column partials [n_chunks][K]; after each of passes 0 and 1 the
+ * ranks exchange partials (all-gather) and wd_resample_phi_reduce folds all
+ * n_chunks partials in chunk order into colstat[2K] (maxima, sums).  Every
+ * rank then holds the same column statistics, its own rows of phi are
+ * bit-identical to wd_resample_phi's, and an all-gather of the rows
+ * completes phi (device_lda.DeviceLDA, sharded resample).
+ */
+int wd_resample_phi_chunks(void);
+int wd_resample_phi_pass(int dtype, int pass, const int32_t* word_topic, int64_t vocab_size, int32_t n_topics,
+                         double beta, uint64_t seed, void* phi, int64_t ld_phi, int chunk0, int chunk1, int n_chunks,
+                         float* partials, const float* colstat, void* stream);
+int wd_resample_phi_reduce(int pass, const float* partials, int n_chunks, int32_t n_topics, float* colstat,
+                           void* stream);
 
 /*
  * log_likelihood (lda.py:289-305): *out = sum over tokens of

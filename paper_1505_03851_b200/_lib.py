@@ -45,6 +45,9 @@ EXPORTS = (
     "wd_l2_read_probe",
     "wd_build_block_tables",
     "wd_butterfly_search",
+    "wd_resample_phi_chunks",
+    "wd_resample_phi_pass",
+    "wd_resample_phi_reduce",
 )
 
 
@@ -101,6 +104,13 @@ def _declare(L):
     L.wd_l2_read_probe.argtypes = [vp, i64, i32, i32, vp, vp]
     L.wd_build_block_tables.restype = i32
     L.wd_build_block_tables.argtypes = [i32, i32, vp, ctypes.c_int32, i64, vp, vp, vp]
+    L.wd_resample_phi_chunks.restype = i32
+    L.wd_resample_phi_chunks.argtypes = []
+    L.wd_resample_phi_pass.restype = i32
+    L.wd_resample_phi_pass.argtypes = [i32, i32, vp, i64, ctypes.c_int32, ctypes.c_double, u64, vp, i64, i32, i32, i32,
+                                       vp, vp, vp]
+    L.wd_resample_phi_reduce.restype = i32
+    L.wd_resample_phi_reduce.argtypes = [i32, vp, i32, ctypes.c_int32, vp, vp]
     L.wd_butterfly_search.restype = i32
     L.wd_butterfly_search.argtypes = [i32, i32, vp, vp, vp, ctypes.c_int32, i64, vp, vp, vp]
 

@@ -229,15 +229,24 @@ __global__ void log_gamma_cells(uint64_t seed, const int64_t* __restrict__ rows,
 // per-CTA column partials reduced in a fixed order (deterministic).
 constexpr int kPhiThreads = 256;
 
+// The V rows are cut into n_chunks fixed row chunks (ceil(V / n_chunks)
+// rows each); CTA i of a launch handles chunk chunk0 + i and writes that
+// chunk's column partials.  The whole matrix is chunk0 = 0 with n_chunks
+// CTAs; a rank of a sharded resample runs its own chunk range -- the same
+// chunks, the same Gamma counters, the same partials, so the result is
+// bit-identical for any number of ranks.
 template <typename T>
 __global__ void __launch_bounds__(kPhiThreads) phi_pass(int pass, const int32_t* __restrict__ wt, int64_t V,
                                                         int32_t K, float beta, uint64_t seed, T* __restrict__ phi,
                                                         int64_t ld, float* __restrict__ part,
-                                                        const float* __restrict__ colstat) {
-  const int64_t rows_per = (V + gridDim.x - 1) / gridDim.x;
-  const int64_t v0 = (int64_t)blockIdx.x * rows_per;
+                                                        const float* __restrict__ colstat, int chunk0, int n_chunks) {
+  const int64_t g = (int64_t)chunk0 + blockIdx.x;
+  const int64_t rows_per = (V + n_chunks - 1) / n_chunks;
+  const int64_t v0 = g * rows_per < V ? g * rows_per : V;
   const int64_t v1 = v0 + rows_per < V ? v0 + rows_per : V;
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+  // gridDim.y column blocks split a chunk's columns (each column, and so its
+  // partial, is still computed by exactly one thread: the same bits)
+  for (int k = blockIdx.y * blockDim.x + threadIdx.x; k < K; k += gridDim.y * blockDim.x) {
     float acc = pass == 0 ? -INFINITY : 0.f;
     const float cs = pass == 0 ? 0.f : colstat[k];
     if (pass == 0) {
@@ -266,7 +275,7 @@ __global__ void __launch_bounds__(kPhiThreads) phi_pass(int pass, const int32_t*
         *p = (T)((float)*p / cs);
       }
     }
-    if (pass < 2) part[(int64_t)blockIdx.x * K + k] = acc;
+    if (pass < 2) part[g * K + k] = acc;
   }
 }
 
@@ -387,11 +396,11 @@ static int resample_phi_t(const int32_t* wt, int64_t V, int32_t K, float beta, u
   float* part = (float*)ws;
   float* colstat = part + (size_t)G * K;
   int cb = (K + 255) / 256;
-  phi_pass<T><<<G, kPhiThreads, 0, st>>>(0, wt, V, K, beta, seed, phi, ld, part, nullptr);
+  phi_pass<T><<<G, kPhiThreads, 0, st>>>(0, wt, V, K, beta, seed, phi, ld, part, nullptr, 0, G);
   col_reduce<<<cb, 256, 0, st>>>(0, part, G, K, colstat);
-  phi_pass<T><<<G, kPhiThreads, 0, st>>>(1, wt, V, K, beta, seed, phi, ld, part, colstat);
+  phi_pass<T><<<G, kPhiThreads, 0, st>>>(1, wt, V, K, beta, seed, phi, ld, part, colstat, 0, G);
   col_reduce<<<cb, 256, 0, st>>>(1, part, G, K, colstat + K);
-  phi_pass<T><<<G, kPhiThreads, 0, st>>>(2, wt, V, K, beta, seed, phi, ld, part, colstat + K);
+  phi_pass<T><<<G, kPhiThreads, 0, st>>>(2, wt, V, K, beta, seed, phi, ld, part, colstat + K, 0, G);
   return ck();
 }
 
@@ -456,6 +465,47 @@ int wd_resample_phi(int dtype, const int32_t* word_topic, int64_t vocab_size, in
     return resample_phi_t<double>(word_topic, vocab_size, n_topics, (float)beta, seed, (double*)phi, ld_phi,
                                   workspace, workspace_bytes, st);
   return WD_ERR_INVALID_ARGUMENT;
+}
+
+int wd_resample_phi_chunks(void) { return phi_grid(); }
+
+int wd_resample_phi_pass(int dtype, int pass, const int32_t* word_topic, int64_t vocab_size, int32_t n_topics,
+                         double beta, uint64_t seed, void* phi, int64_t ld_phi, int chunk0, int chunk1, int n_chunks,
+                         float* partials, const float* colstat, void* stream) {
+  if (pass < 0 || pass > 2 || vocab_size <= 0 || n_topics <= 0 || !word_topic || !phi || ld_phi < n_topics ||
+      beta <= 0 || n_chunks <= 0 || chunk0 < 0 || chunk1 > n_chunks || chunk0 > chunk1 || !partials ||
+      (pass > 0 && !colstat))
+    return WD_ERR_INVALID_ARGUMENT;
+  if (chunk1 == chunk0) return WD_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  // pass 1 reads the column maxima (colstat[0, K)), pass 2 the sums (colstat[K, 2K))
+  const float* cs = pass == 0 ? nullptr : (pass == 1 ? colstat : colstat + n_topics);
+  // a rank's share of the chunks alone would leave SMs idle: its columns
+  // are split over enough CTAs to cover the GPU
+  int cols = (n_topics + wd::kPhiThreads - 1) / wd::kPhiThreads;
+  const int want = wd::phi_grid();
+  int ysplit = 1;
+  while (ysplit < cols && (chunk1 - chunk0) * ysplit < want) ysplit *= 2;
+  if (ysplit > cols) ysplit = cols;
+  const dim3 grid(chunk1 - chunk0, ysplit);
+  if (dtype == WD_FLOAT32)
+    wd::phi_pass<float><<<grid, wd::kPhiThreads, 0, st>>>(pass, word_topic, vocab_size, n_topics, (float)beta, seed,
+                                                          (float*)phi, ld_phi, partials, cs, chunk0, n_chunks);
+  else if (dtype == WD_FLOAT64)
+    wd::phi_pass<double><<<grid, wd::kPhiThreads, 0, st>>>(pass, word_topic, vocab_size, n_topics, (float)beta, seed,
+                                                           (double*)phi, ld_phi, partials, cs, chunk0, n_chunks);
+  else
+    return WD_ERR_INVALID_ARGUMENT;
+  return wd::ck();
+}
+
+int wd_resample_phi_reduce(int pass, const float* partials, int n_chunks, int32_t n_topics, float* colstat,
+                           void* stream) {
+  if ((pass != 0 && pass != 1) || !partials || !colstat || n_chunks <= 0 || n_topics <= 0)
+    return WD_ERR_INVALID_ARGUMENT;
+  wd::col_reduce<<<(n_topics + 255) / 256, 256, 0, (cudaStream_t)stream>>>(pass, partials, n_chunks, n_topics,
+                                                                          colstat + (pass == 0 ? 0 : n_topics));
+  return wd::ck();
 }
 
 int wd_log_likelihood(int dtype, const void* theta, int64_t ld_theta, const void* phi, int64_t ld_phi,

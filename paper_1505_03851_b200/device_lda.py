@@ -19,6 +19,8 @@ run is independent of the number of GPUs (tests/test_multigpu.py).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -66,7 +68,27 @@ class DeviceLDA:
         self.device = dev
         # line-aligned W-topic blocks (kernels.block_aligned_rows)
         self.theta = theta if theta is not None else block_aligned_rows(corpus.n_docs, self.K, self.dtype, dev, lanes)
-        self.phi = phi if phi is not None else block_aligned_rows(self.V, self.K, self.dtype, dev, lanes)
+        # sharded phi resample (multi-GPU): each rank resamples a fixed share
+        # of the row chunks and the rows are all-gathered (resample()).  The
+        # phi rows then live in a padded [chunks x rows_per, ld] buffer whose
+        # rank slices are contiguous; phi is its [V, K] view.
+        L0 = _lib.load()
+        self._phi_chunks = int(L0.wd_resample_phi_chunks())
+        world = self.torch.distributed.get_world_size(process_group) if process_group is not None else 1
+        self.world = world
+        self.rank = self.torch.distributed.get_rank(process_group) if process_group is not None else 0
+        self.shard_phi = (phi is None and world > 1 and self._phi_chunks % world == 0 and
+                          os.environ.get("WD_SHARD_PHI", "1") != "0")
+        if self.shard_phi:
+            rows_per = -(-self.V // self._phi_chunks)
+            self._phi_rows_pad = rows_per * self._phi_chunks
+            base_view = block_aligned_rows(self._phi_rows_pad, self.K, self.dtype, dev, lanes)
+            self._phi_base = base_view._base if base_view._base is not None else base_view
+            self.phi = base_view[: self.V]
+            self._phi_part = torch.empty((self._phi_chunks, self.K), dtype=torch.float32, device=dev)
+            self._phi_colstat = torch.empty(2 * self.K, dtype=torch.float32, device=dev)
+        else:
+            self.phi = phi if phi is not None else block_aligned_rows(self.V, self.K, self.dtype, dev, lanes)
         self.z = torch.zeros(corpus.n_tokens, dtype=torch.int32, device=dev)
         self.word_topic = torch.zeros((self.V, self.K), dtype=torch.int32, device=dev)
         L = _lib.load()
@@ -161,21 +183,61 @@ class DeviceLDA:
         if self.pg is not None and getattr(self, "_reducer", None) is None:
             self.torch.distributed.all_reduce(self.word_topic, group=self.pg)
 
+    def _resample_theta(self, t: int):
+        L = _lib.load()
+        _lib.check(L.wd_resample_theta(self._dt, self.z.data_ptr(), self.corpus.offsets.data_ptr(),
+                                       self.corpus.n_docs, self.K, self.alpha, derive_seed(self.seed, 2, t, 0),
+                                       self.corpus.doc_base, self.theta.data_ptr(), self.theta.stride(0),
+                                       _lib.stream_handle()), "wd_resample_theta")
+
+    def _all_gather_slices(self, buf, async_op=False):
+        """In-place all-gather of equal contiguous rank slices of `buf` (rank r
+        owns elements [r*n/world, (r+1)*n/world))."""
+        dist = self.torch.distributed
+        flat = buf.view(-1)
+        n = flat.numel() // self.world
+        mine = flat[self.rank * n:(self.rank + 1) * n]
+        if dist.get_backend(self.pg) == "nccl":
+            return dist.all_gather_into_tensor(flat, mine, group=self.pg, async_op=async_op)
+        return dist.all_gather(list(flat.split(n)), mine.clone(), group=self.pg, async_op=async_op)
+
     def resample(self, t: int):
         L = _lib.load()
         st = _lib.stream_handle()
-        # theta needs only the local z: it runs while in-flight count
-        # all-reduces finish; phi waits for them
-        _lib.check(L.wd_resample_theta(self._dt, self.z.data_ptr(), self.corpus.offsets.data_ptr(),
-                                       self.corpus.n_docs, self.K, self.alpha, derive_seed(self.seed, 2, t, 0),
-                                       self.corpus.doc_base, self.theta.data_ptr(), self.theta.stride(0), st),
-                   "wd_resample_theta")
+        if not self.shard_phi:
+            # theta needs only the local z: it runs while in-flight count
+            # all-reduces finish; phi waits for them
+            self._resample_theta(t)
+            if getattr(self, "_reducer", None) is not None:
+                self._reducer.wait()
+                self._reducer = None
+            _lib.check(L.wd_resample_phi(self._dt, self.word_topic.data_ptr(), self.V, self.K, self.beta,
+                                         derive_seed(self.seed, 2, t, 1), self.phi.data_ptr(), self.phi.stride(0),
+                                         self._phi_ws.data_ptr(), self._phi_ws.numel(), st), "wd_resample_phi")
+            return
+        # Sharded phi (DESIGN section 6): this rank's share of the fixed row
+        # chunks, column partials exchanged after passes 0 and 1 (all-gather,
+        # folded in chunk order: the same bits on every rank and for any
+        # world size), then the rows all-gathered on the NCCL stream WHILE
+        # theta resamples on this one.
         if getattr(self, "_reducer", None) is not None:
             self._reducer.wait()
             self._reducer = None
-        _lib.check(L.wd_resample_phi(self._dt, self.word_topic.data_ptr(), self.V, self.K, self.beta,
-                                     derive_seed(self.seed, 2, t, 1), self.phi.data_ptr(), self.phi.stride(0),
-                                     self._phi_ws.data_ptr(), self._phi_ws.numel(), st), "wd_resample_phi")
+        G = self._phi_chunks
+        c0, c1 = self.rank * G // self.world, (self.rank + 1) * G // self.world
+        seed = derive_seed(self.seed, 2, t, 1)
+        for pss in (0, 1, 2):
+            _lib.check(L.wd_resample_phi_pass(self._dt, pss, self.word_topic.data_ptr(), self.V, self.K, self.beta,
+                                              seed, self.phi.data_ptr(), self.phi.stride(0), c0, c1, G,
+                                              self._phi_part.data_ptr(), self._phi_colstat.data_ptr(), st),
+                       "wd_resample_phi_pass")
+            if pss < 2:
+                self._all_gather_slices(self._phi_part)
+                _lib.check(L.wd_resample_phi_reduce(pss, self._phi_part.data_ptr(), G, self.K,
+                                                    self._phi_colstat.data_ptr(), st), "wd_resample_phi_reduce")
+        work = self._all_gather_slices(self._phi_base, async_op=True)
+        self._resample_theta(t)
+        work.wait()
 
     def iterate(self, t: int, overlap_allreduce: bool = True):
         self.draw(t, overlap_allreduce=overlap_allreduce)

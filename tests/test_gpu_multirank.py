@@ -56,18 +56,24 @@ def _run(rank, world, port, out_dir, iters):
     lda.check_errors()
     ll = lda.log_likelihood()
     np.savez(os.path.join(out_dir, f"r{world}_{rank}.npz"), z=lda.z.cpu().numpy(), theta=lda.theta.cpu().numpy(),
-             phi=lda.phi.cpu().numpy(), wt=lda.word_topic.cpu().numpy(), ll=np.array(ll))
+             phi=lda.phi.cpu().numpy(), wt=lda.word_topic.cpu().numpy(), ll=np.array(ll),
+             sharded=np.array(lda.shard_phi))
     if world > 1:
         dist.destroy_process_group()
 
 
-def test_two_ranks_reproduce_one(tmp_path):
+@pytest.mark.parametrize("world", [2, 4])
+def test_ranks_reproduce_one(tmp_path, world):
+    """N > 1 runs the sharded phi resample (each rank its share of the row
+    chunks, column partials and rows all-gathered): phi must still be the
+    1-rank phi bit for bit, and with it the whole chain."""
     iters = 3
     _run(0, 1, 0, str(tmp_path), iters)
-    mp.start_processes(_run, args=(2, _free_port(), str(tmp_path), iters), nprocs=2, join=True,
+    mp.start_processes(_run, args=(world, _free_port(), str(tmp_path), iters), nprocs=world, join=True,
                        start_method="spawn")
     one = np.load(tmp_path / "r1_0.npz")
-    parts = [np.load(tmp_path / f"r2_{r}.npz") for r in range(2)]
+    parts = [np.load(tmp_path / f"r{world}_{r}.npz") for r in range(world)]
+    assert all(bool(p["sharded"]) for p in parts)
     np.testing.assert_array_equal(np.concatenate([p["z"] for p in parts]), one["z"])
     np.testing.assert_array_equal(np.concatenate([p["theta"] for p in parts]), one["theta"])
     for p in parts:

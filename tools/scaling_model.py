@@ -9,8 +9,14 @@ events.  A rank's iteration at N GPUs is then
 
     T_N = draw_N + theta_N + phi + allreduce_tail_N
 
-where phi (V x K, every rank resamples it identically) does not shrink with
-N, and the count all-reduce is hidden behind the next vocabulary tile's draw
+with phi resampled whole on every rank ("replicated_phi"), or sharded
+("sharded_phi", DeviceLDA's default for N > 1):
+
+    T_N = draw_N + allreduce_tail_N + phi_share_N + 2 partial all-gathers
+          + max(theta_N, phi rows all-gather)
+
+(the rows' all-gather runs on the NCCL stream while theta resamples).  The
+count all-reduce is hidden behind the next vocabulary tile's draw
 except the LAST tile's rows (DeviceLDA draw(overlap_allreduce=True)), whose
 all-reduce is exposed: bytes = (V / tiles) x K x 4, time = 2 (N-1)/N x bytes
 / busbw (ring all-reduce), busbw an assumption given on the command line
@@ -70,9 +76,28 @@ def time_shard(args, rank, world, dev):
         e[3].record(st)
     torch.cuda.synchronize()
     mean = lambda i, j: sum(x[i].elapsed_time(x[j]) for x in ev) / len(ev)  # noqa: E731
+    # the sharded phi resample's compute on this rank: its 1/world share of
+    # the fixed row chunks, three passes (+ the two column-partial folds)
+    G = int(L.wd_resample_phi_chunks())
+    c0, c1 = rank * G // world, (rank + 1) * G // world
+    part = torch.empty((G, lda.K), dtype=torch.float32, device=dev)
+    colstat = torch.zeros(2 * lda.K, dtype=torch.float32, device=dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for s in range(args.steps):
+        for pss in (0, 1, 2):
+            _lib.check(L.wd_resample_phi_pass(lda._dt, pss, lda.word_topic.data_ptr(), lda.V, lda.K, lda.beta, 99 + s,
+                                              lda.phi.data_ptr(), lda.phi.stride(0), c0, c1, G, part.data_ptr(),
+                                              colstat.data_ptr(), _lib.stream_handle()), "phi pass")
+            if pss < 2:
+                _lib.check(L.wd_resample_phi_reduce(pss, part.data_ptr(), G, lda.K, colstat.data_ptr(),
+                                                    _lib.stream_handle()), "phi reduce")
+    b.record(st)
+    torch.cuda.synchronize()
     out = {"rank": rank, "docs": dc.n_docs, "tokens": dc.n_tokens, "draw_ms": mean(0, 1), "theta_ms": mean(1, 2),
            "phi_ms": mean(2, 3), "iter_ms": mean(0, 3), "vocab_tiles": lda.tiles.n_tiles,
-           "rows_per_tile": lda.tiles.rows_per_tile}
+           "rows_per_tile": lda.tiles.rows_per_tile, "phi_shard_ms": a.elapsed_time(b) / args.steps,
+           "phi_bytes": (-(-lda.V // G) * G) * lda.phi.stride(0) * lda.phi.element_size()}
     del lda, dc
     torch.cuda.empty_cache()
     return out
@@ -82,6 +107,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--busbw-gbs", type=float, default=700.0)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--collective-latency-us", type=float, default=25.0,
+                    help="latency of one small (2.4 MB) all-gather of column partials")
     ap.add_argument("--docs", type=int, default=1_000_000)
     ap.add_argument("--topics", type=int, default=1024)
     ap.add_argument("--vocab", type=int, default=40_000)
@@ -103,9 +130,20 @@ def main():
             t1 = t_n
         if N == 1:
             total_tokens = shards[0]["tokens"]
-        res["per_n"][N] = {"shards": shards, "exposed_allreduce_ms": ar_ms, "predicted_iter_ms": t_n,
-                           "predicted_tokens_per_s": total_tokens / (t_n / 1e3),
-                           "predicted_efficiency": t1 / (N * t_n)}
+        # sharded phi (DeviceLDA default for N > 1): the rank's phi share, two
+        # column-partial all-gathers (~latency), then the rows' all-gather
+        # overlapping the theta resample
+        ag_ms = 0.0 if N == 1 else (N - 1) / N * worst["phi_bytes"] / (args.busbw_gbs * 1e9) * 1e3
+        part_ms = 0.0 if N == 1 else 2 * args.collective_latency_us / 1e3
+        t_sh = (worst["draw_ms"] + ar_ms + worst["phi_shard_ms"] + part_ms + max(worst["theta_ms"], ag_ms)
+                if N > 1 else t_n)
+        res["per_n"][N] = {"shards": shards, "exposed_allreduce_ms": ar_ms,
+                           "replicated_phi": {"predicted_iter_ms": t_n, "predicted_tokens_per_s": total_tokens / (t_n / 1e3),
+                                              "predicted_efficiency": t1 / (N * t_n)},
+                           "sharded_phi": {"phi_allgather_ms": ag_ms, "partials_allgather_ms": part_ms,
+                                           "predicted_iter_ms": t_sh,
+                                           "predicted_tokens_per_s": total_tokens / (t_sh / 1e3),
+                                           "predicted_efficiency": t1 / (N * t_sh)}}
     print(json.dumps(res))
 
 
