@@ -70,14 +70,15 @@ def timed(fn, n, warm=2):
     return a.elapsed_time(b) / 1e3 / n
 
 
-def run(name, peak, run_pad=None, dtype="float32", lanes=32):
+def run(name, peak, run_pad=None, dtype="float32", lanes=32, tile_mb=None):
     M, V, K, mean, kind, iters = CONFIGS[name]
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(2026)
     off, words = make_corpus(M, V, mean, kind, g, dev)
     dc = wd.DeviceCorpus.from_csr(off, words, vocab_size=V)
     T = dc.n_tokens
-    lda = DeviceLDA(dc, K, V, seed=2026, run_pad=run_pad, dtype=getattr(torch, dtype), lanes=lanes)
+    kw = {} if tile_mb is None else {"vocab_tile_bytes": int(tile_mb * (1 << 20))}
+    lda = DeviceLDA(dc, K, V, seed=2026, run_pad=run_pad, dtype=getattr(torch, dtype), lanes=lanes, **kw)
     lda.init_uniform()
     it = [0]
 
@@ -117,6 +118,7 @@ def main():
     ap.add_argument("--only", default=",".join(CONFIGS))
     ap.add_argument("--out", default="gpurun_out/configs.json")
     ap.add_argument("--run-pad", type=int, default=None, help="force VocabTiles.run_pad (default: DeviceLDA's rule)")
+    ap.add_argument("--tile-mb", type=float, default=None, help="vocabulary tile size (default: DeviceLDA's 40 MB)")
     ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
     ap.add_argument("--lanes", type=int, default=32)
     args = ap.parse_args()
@@ -127,7 +129,7 @@ def main():
     out = []
     for name in args.only.split(","):
         t0 = time.time()
-        r = run(name, peak, args.run_pad, args.dtype, args.lanes)
+        r = run(name, peak, args.run_pad, args.dtype, args.lanes, args.tile_mb)
         r["wall_s"] = time.time() - t0
         print(json.dumps(r), flush=True)
         out.append(r)
