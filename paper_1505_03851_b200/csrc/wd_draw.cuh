@@ -158,6 +158,31 @@ __device__ __forceinline__ T make_stop(const DrawParams<T>& p, int64_t tok, T to
   return stop;
 }
 
+// make_stop in two halves, so the 64-bit u hash can run before pass 1 (its
+// keys do not depend on the products) and overlap the block loads:
+// stop_pre = fl_T(u) (or the explicit stop), stop_finish(pre, total) = the
+// same value make_stop returns.
+template <typename T>
+__device__ __forceinline__ T stop_pre(const DrawParams<T>& p, int64_t tok, uint64_t ka, uint64_t kb, bool rows) {
+  if (p.stop_mode == WD_STOPS_EXPLICIT) return p.stops[tok];
+  if (p.stop_mode == WD_STOPS_UNITS) return from_double<T>(p.units[tok]);
+  if (p.stop_mode == WD_STOPS_PHILOX) return unit_to<T>(philox_bits(p.seed, ka, kb));
+  return unit_to<T>(rows ? unit_bits1(p.seed, ka) : unit_bits2(p.seed, ka, kb));
+}
+template <typename T>
+__device__ __forceinline__ T stop_finish(const DrawParams<T>& p, T pre, T total) {
+  if (p.stop_mode == WD_STOPS_EXPLICIT) {
+    const T stop = pre;
+    bool live = total > T(0);
+    if (stop < T(0) || (live && stop >= total) || (!live && stop > T(0))) atomicAnd(p.err + 1, 0ull);
+    return stop;
+  }
+  T stop = mul_rn(total, pre);
+  if (!(total > T(0))) return T(0);
+  if (stop >= total) stop = next_below(total);
+  return stop;
+}
+
 // ============================================================== butterfly
 // cp.async (LDGSTS): 16-byte global -> shared copies that hold no registers
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {

@@ -34,6 +34,9 @@
 
 namespace wd {
 
+#ifndef WD_SMALL_EARLY
+#define WD_SMALL_EARLY 0  // measured at K = 200: 14.8 vs 13.6 ms (register pressure)
+#endif
 #ifndef WD_SMALL_LDA_MIN_BLOCKS  // measured at K = 200: 5 / 6 / 7 / 8 CTAs per SM -> 13.85 / 13.58 / 13.82 / 15.07 ms
 #define WD_SMALL_LDA_MIN_BLOCKS 6
 #endif
@@ -103,6 +106,18 @@ __global__ void __launch_bounds__(128, WD_SMALL_LDA_MIN_BLOCKS) lda_small_kernel
     }
     const float prem = acc;
 
+    // the own token's keys and u (or explicit stop) before pass 1: the hash
+    // chain and the key loads overlap the block loads (WD_SMALL_EARLY)
+    uint64_t ka = 0, kb = 0;
+    unsigned long long ekey = 0;
+    int r = 0;
+    int64_t zidx = 0;
+    float pre = 0.f;
+    if (WD_SMALL_EARLY && own_valid) {
+      token_keys<float, MODE_LDA>(p, tok0 + own, own_doc, W, ka, kb, ekey, r, zidx);
+      pre = stop_pre<float>(p, zidx, ka, kb, false);
+    }
+
     // ---- pass 1: block totals of the own row, T8 stash, running sums in registers
     float S[NB];
     const bool fast = __all_sync(FULL, single);
@@ -160,12 +175,11 @@ __global__ void __launch_bounds__(128, WD_SMALL_LDA_MIN_BLOCKS) lda_small_kernel
 
     // ---- pass 2 (own row)
     if (own_valid) {
-      uint64_t ka, kb;
-      unsigned long long ekey;
-      int r;
-      int64_t zidx;
-      token_keys<float, MODE_LDA>(p, tok0 + own, own_doc, W, ka, kb, ekey, r, zidx);
-      const float stop = make_stop<float>(p, zidx, total, ka, kb, false);
+      if (!WD_SMALL_EARLY) {
+        token_keys<float, MODE_LDA>(p, tok0 + own, own_doc, W, ka, kb, ekey, r, zidx);
+        pre = stop_pre<float>(p, zidx, ka, kb, false);
+      }
+      const float stop = stop_finish<float>(p, pre, total);
       const bool live = total > 0.f;
       if (!live) atomicMin(p.err, ekey);
       int j = 0;  // first block whose running sum exceeds stop (nb - 1 if none)
