@@ -38,6 +38,9 @@ namespace wd {
 #ifndef WD_LEAN_MIN_BLOCKS
 #define WD_LEAN_MIN_BLOCKS 8
 #endif
+#ifndef WD_LEAN_PIPE2
+#define WD_LEAN_PIPE2 0
+#endif
 #ifndef WD_LEAN_NBC
 #define WD_LEAN_NBC 32  // running sums kept per lane (4 KB of S per warp)
 #endif
@@ -163,6 +166,21 @@ __global__ void __launch_bounds__(128, MINB) lda_lean_kernel(DrawParams<float> p
       th1.idx[0] = (uint32_t)(d1 < 0 ? (int32_t)trow.idx[0] : d1);
       const int pf = p.theta_prefetch;
       const char* tpf = th1.base + (uint64_t)th1.idx[0] * th1.ldb;  // the lane's theta row (segment s)
+#if WD_LEAN_PIPE2
+      // two blocks in flight per warp: block b+1's loads issued before block
+      // b's arithmetic (needs ~100 registers: 5 CTAs per SM)
+      Regs cur;
+      if (nb > 0) cur.load(prow, th1, 0, pol_x, pol_t);
+      for (int b = 0; b < nb; ++b) {
+        Regs nxt;
+        if (b + 1 < nb) nxt.load(prow, th1, (int64_t)(b + 1) * W, pol_x, pol_t);
+        const float t = cur.reduce(rvalid, s, 0u);
+        acc = add_rn(acc, t);
+        store_s(S, b, nb, G, lane, acc);
+        cur = nxt;
+      }
+      if (false)
+#endif
 #pragma unroll 2
       for (int b = 0; b < nb; ++b) {
         Regs cur;

@@ -384,18 +384,23 @@ def test_vocab_tiled_draw_identical(kernel, run_pad):
     np.testing.assert_array_equal(z, exp)
 
 
-@pytest.mark.parametrize("words_kind", ["uniform", "zipf"])
-def test_full_size_lda_k1024_sampled_tokens(words_kind):
-    """The bench shape (BASELINE configs[3] per GPU: 1M documents, Poisson(200)
-    lengths, V=40k, K=1024, vocabulary-tiled, (document, word)-ordered and
-    run-padded), uniform and Zipf words: 4096 randomly chosen tokens are
-    re-drawn one by one by the oracle from the same theta/phi rows, u and
-    master-index key, and must match bit-for-bit; the fused word-topic counts
-    must sum to the token count."""
+@pytest.mark.parametrize("K,M,words_kind,tiles", [(1024, 1_000_000, "uniform", 4), (1024, 1_000_000, "zipf", 4),
+                                                   (200, 1_000_000, "zipf", 1), (2048, 1_000_000, "uniform", 8),
+                                                   (4096, 1_250_016, "uniform", 16)])
+def test_full_size_lda_sampled_tokens(K, M, words_kind, tiles):
+    """The BASELINE shapes at full size through DeviceLDA (vocabulary-tiled,
+    (document, word)-ordered, run-padded): configs[3] per GPU (1M documents,
+    Poisson(200) lengths, V=40k, K=1024) uniform and Zipf; configs[2]
+    Wikipedia-shaped (K=200, Zipf words: the small-K kernel); K=2048 and one
+    rank's shard of configs[4] (1.25M documents, K=4096: the register-lean
+    kernel).  4096 randomly chosen tokens are re-drawn one by one by the
+    oracle from the same theta/phi rows, u and master-index key, and must
+    match bit-for-bit; the fused word-topic counts must sum to the token
+    count."""
     from paper_1505_03851_b200.device_lda import DeviceLDA
 
-    g = torch.Generator(device="cuda").manual_seed(3)
-    M, V, K = 1_000_000, 40_000, 1024
+    g = torch.Generator(device="cuda").manual_seed(3 + K)
+    V = 40_000
     lengths = torch.poisson(torch.full((M,), 200.0, device="cuda"), generator=g).clamp_(min=1).long()
     off = torch.zeros(M + 1, dtype=torch.int64, device="cuda")
     off[1:] = torch.cumsum(lengths, 0)
@@ -410,7 +415,7 @@ def test_full_size_lda_k1024_sampled_tokens(words_kind):
     dc = wd.DeviceCorpus.from_csr(off, words)
     lda = DeviceLDA(dc, K, V, seed=11)
     lda.init_uniform()
-    assert lda.tiles is not None and lda.tiles.n_tiles == 4 and lda.tiles.run_pad == 4
+    assert lda.tiles is not None and lda.tiles.n_tiles == tiles and lda.tiles.run_pad == 4
     lda.draw(0)
     lda.check_errors()
     assert int(lda.word_topic.sum()) == T
