@@ -276,6 +276,49 @@ def _python_ref_worker(job):
     return int(N.sum()), time.perf_counter() - t0
 
 
+def _python_ref_basic_worker(job):
+    """One process: the reference's draw_z_basic (kernels.py:380-401: per
+    word products, np.cumsum, bisection) on one 32-document group."""
+    ref, K, V, mean, seed, idx = job
+    sys.path.insert(0, ref)
+    import numpy as np
+    from warpdraw.kernels import SeededStops, draw_z_basic
+
+    g = np.random.default_rng(seed + idx)
+    N = np.maximum(g.poisson(mean, size=32), 1).astype(np.int64)
+    w = [g.integers(0, V, size=int(n)) for n in N]
+    theta = g.uniform(0.1, 1.0, size=(32, K)).astype(np.float32)
+    phi = g.uniform(0.1, 1.0, size=(V, K)).astype(np.float32)
+    t0 = time.perf_counter()
+    draw_z_basic(N, theta, phi, w, SeededStops(seed))
+    return int(N.sum()), time.perf_counter() - t0
+
+
+def python_reference_rows(K, rows, seed):
+    """configs[1] on the CPU the reference's way: the batched
+    emulator build_block_tables + butterfly_search (kernels.py:580-600,
+    317-362) over `rows` independent fp32 rows, one process; draws/s."""
+    ref = _reference_package()
+    if ref is None:
+        return None
+    sys.path.insert(0, ref)
+    import numpy as np
+    from warpdraw import rng as R
+    from warpdraw.kernels import _stops_from_units, build_block_tables, butterfly_search
+    from warpdraw.warp import WarpConfig
+
+    g = np.random.default_rng(seed)
+    w = g.uniform(0.1, 1.0, size=(rows // 32, 32, K)).astype(np.float32)
+    t0 = time.perf_counter()
+    warp, p, sums = build_block_tables(w, WarpConfig(32, 4))
+    u = R.units_for(R.derive_seed(seed, 6), np.arange(sums.size)).reshape(sums.shape)
+    butterfly_search(warp, p, sums, _stops_from_units(sums, u, np.float32))
+    dt = time.perf_counter() - t0
+    return {"draws_per_s": rows / dt, "rows": rows, "seconds": dt, "processes": 1,
+            "sample": f"warpdraw.kernels.build_block_tables + butterfly_search (reference, batched emulator) on "
+                      f"{rows} rows x K={K} fp32, W=32, one process"}
+
+
 def python_reference(args, cores):
     """the reference's own draw_z_butterfly (fp32, W = 32,
     SeededStops) on 1 process and on C processes (multiprocessing, disjoint
@@ -294,8 +337,16 @@ def python_reference(args, cores):
         res = pool.map(_python_ref_worker, [job[:-1] + (i,) for i in range(procs)])
     wall = time.perf_counter() - t0
     ntok = sum(r[0] for r in res)
+    nb1, db1 = _python_ref_basic_worker(job)
+    t0 = time.perf_counter()
+    with ctx.Pool(procs) as pool:
+        resb = pool.map(_python_ref_basic_worker, [job[:-1] + (i,) for i in range(procs)])
+    wallb = time.perf_counter() - t0
     return {"single_process_tokens_per_s": ntok1 / dt1, "processes": procs,
             "multiprocess_tokens_per_s": ntok / wall,
+            "basic": {"single_process_tokens_per_s": nb1 / db1,
+                      "multiprocess_tokens_per_s": sum(r[0] for r in resb) / wallb,
+                      "sample": "warpdraw.kernels.draw_z_basic (reference) fp32, one 32-document group per process"},
             "sample": f"warpdraw.kernels.draw_z_butterfly (reference, {ref}) fp32 W=32 K={args.topics} V={args.vocab}:"
                       f" one 32-document group (Poisson({args.mean_len:g})) per process; 1 process {ntok1} tokens in "
                       f"{dt1:.1f}s; {procs} processes {ntok} tokens in {wall:.1f}s wall"}
@@ -636,6 +687,23 @@ def main():
             "prefix_table_draws_per_s": n / res["prefix"],
             "speedup_vs_prefix_table": res["prefix"] / res["butterfly"],
         }
+        if not args.no_cpu:
+            # configs[1] on the host: the oracle C port on all threads, and the
+            # reference's own batched emulator on one process (bounded samples)
+            from oracle import oracle as O
+            import numpy as np
+
+            cores = len(os.sched_getaffinity(0))
+            rows_c = 1 << 16
+            wh = np.random.default_rng(1).uniform(0.1, 1.0, size=(rows_c, K)).astype(np.float32)
+            t0 = time.perf_counter()
+            O.sample_rows(wh, 32, 5, threads=cores)
+            dtc = time.perf_counter() - t0
+            sampler["cpu_baseline"] = {
+                "value": rows_c / dtc, "unit": "draws/s", "cores": cores, "kind": "port",
+                "sample": f"oracle/wd_oracle.c sample_rows on {rows_c} rows x K={K} fp32, {cores} threads",
+                "python_reference": python_reference_rows(K, 16384, 5)}
+            del wh
         del wts, out
 
     del lda
