@@ -55,6 +55,10 @@ extern "C" {
 /* element type of theta / phi / weights / explicit stops */
 #define WD_FLOAT32 0
 #define WD_FLOAT64 1
+/* wd_draw_z only: float32 theta (and table, explicit stops) with float64 phi;
+ * every product is fl32(fl64(theta * phi)) as the reference's numpy
+ * promotion forms it (kernels.py:209, 391) */
+#define WD_FLOAT32_PHI64 2
 
 /* table variant */
 #define WD_BUTTERFLY 0 /* draw_z_butterfly (kernels.py:487-539)                 */

@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "_lib", "libwarpdraw_b200.so")
 
 WD_OK = 0
-WD_FLOAT32, WD_FLOAT64 = 0, 1
+WD_FLOAT32, WD_FLOAT64, WD_FLOAT32_PHI64 = 0, 1, 2
 WD_BUTTERFLY, WD_PREFIX = 0, 1
 WD_STOPS_SEEDED, WD_STOPS_UNITS, WD_STOPS_EXPLICIT, WD_STOPS_PHILOX = 0, 1, 2, 3
 WD_KEYS_MASTER, WD_KEYS_POSITION = 0, 1

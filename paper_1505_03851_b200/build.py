@@ -24,7 +24,7 @@ INCLUDE = os.path.join(ROOT, "include")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.environ.get("WD_LIB_OUT") or os.path.join(OUT_DIR, "libwarpdraw_b200.so")
 SOURCES = ["wd_draw_f32.cu", "wd_draw_f64.cu", "wd_capi.cu", "wd_resample.cu", "wd_stream.cu", "wd_probe.cu",
-           "wd_table.cu"]
+           "wd_table.cu", "wd_mixed.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # sources whose results are statistical (device resample, log-likelihood)
 STATISTICAL_SOURCES = {"wd_resample.cu"}

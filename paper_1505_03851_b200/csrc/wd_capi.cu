@@ -15,6 +15,7 @@ namespace wd {
 template <typename T>
 int launch_draw(int variant, int W, int vec, int mode, const DrawParams<T>& p, void* ws,
                 size_t ws_bytes, cudaStream_t st);
+int launch_draw_mixed(int variant, int W, const DrawParams<float>& p, cudaStream_t st);
 extern template int launch_draw<float>(int, int, int, int, const DrawParams<float>&, void*, size_t,
                                        cudaStream_t);
 extern template int launch_draw<double>(int, int, int, int, const DrawParams<double>&, void*, size_t,
@@ -201,8 +202,9 @@ int wd_draw_z(int variant, int dtype, int lanes, const void* theta, int64_t ld_t
               const void* stops, int32_t* z, int32_t* word_topic, int32_t* doc_topic, uint64_t* err,
               void* workspace, size_t workspace_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (!valid_lanes(lanes) || (dtype != WD_FLOAT32 && dtype != WD_FLOAT64) || n_topics <= 0 || n_tokens < 0 ||
-      n_docs < 0 || doc_base < 0 || (variant != WD_BUTTERFLY && variant != WD_PREFIX))
+  if (!valid_lanes(lanes) || (dtype != WD_FLOAT32 && dtype != WD_FLOAT64 && dtype != WD_FLOAT32_PHI64) ||
+      n_topics <= 0 || n_tokens < 0 || n_docs < 0 || doc_base < 0 ||
+      (variant != WD_BUTTERFLY && variant != WD_PREFIX))
     return WD_ERR_INVALID_ARGUMENT;
   if (stop_mode < WD_STOPS_SEEDED || stop_mode > WD_STOPS_PHILOX) return WD_ERR_INVALID_ARGUMENT;
   if (key_rule != WD_KEYS_MASTER && key_rule != WD_KEYS_POSITION) return WD_ERR_INVALID_ARGUMENT;
@@ -243,6 +245,12 @@ int wd_draw_z(int variant, int dtype, int lanes, const void* theta, int64_t ld_t
     auto p = make_params<float>();
     fill(p);
     return draw_common<float>(variant, lanes, MODE_LDA, p, workspace, workspace_bytes, st);
+  }
+  if (dtype == WD_FLOAT32_PHI64) {  // p.phi carries the float64 rows (wd_mixed.cu)
+    auto p = make_params<float>();
+    fill(p);
+    const int rc = launch_draw_mixed(variant, lanes, p, st);
+    return rc;
   }
   auto p = make_params<double>();
   fill(p);

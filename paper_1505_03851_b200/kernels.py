@@ -514,7 +514,12 @@ def draw_z_device(kernel: str, corpus: DeviceCorpus, theta, phi, stops, lanes: i
     if needs_pad and (corpus.n_docs % lanes or corpus.doc_base % lanes):
         raise ValueError("document count must be a multiple of the lane count (pad upstream)")
     _lib.require_cuda()
-    if theta.dtype != phi.dtype:
+    # float32 theta with float64 phi: the reference forms fl32(fl64(theta *
+    # phi)) (numpy promotion, kernels.py:209, 391) -- a dedicated path keeps
+    # phi in float64 (csrc/wd_mixed.cu); float64 theta with float32 phi is
+    # exact after widening phi
+    mixed = theta.dtype == torch.float32 and phi.dtype == torch.float64
+    if theta.dtype != phi.dtype and not mixed:
         phi = phi.to(theta.dtype)
     if theta.stride(-1) != 1 or phi.stride(-1) != 1:
         raise ValueError("theta/phi rows must be contiguous")
@@ -524,7 +529,7 @@ def draw_z_device(kernel: str, corpus: DeviceCorpus, theta, phi, stops, lanes: i
     if theta.shape[0] < corpus.n_docs:
         raise ValueError("theta has fewer rows than the corpus has documents")
     dev = theta.device
-    dt = _dtype_code(theta)
+    dt = _lib.WD_FLOAT32_PHI64 if mixed else _dtype_code(theta)
     mode, seed, units = _stop_args(stops, corpus, key_rule, lanes, dev)
     if mode == _lib.WD_STOPS_UNITS and units.numel() < corpus.n_tokens:
         raise ValueError("units do not cover every token")
@@ -543,7 +548,7 @@ def draw_z_device(kernel: str, corpus: DeviceCorpus, theta, phi, stops, lanes: i
     err2.fill_(-1)
     corpus.check_words(int(phi.shape[0]))
     last_key = corpus.last_key(lanes) if (mode == _lib.WD_STOPS_SEEDED and key_rule == _lib.WD_KEYS_MASTER) else None
-    ws, ws_bytes = _workspace(variant, dt, lanes, K, dev)
+    ws, ws_bytes = (None, 0) if mixed else _workspace(variant, dt, lanes, K, dev)
     L = _lib.load()
     st = _lib.stream_handle(stream)
     for li, (wds, tdoc, tpos, a, n, t) in enumerate(launches):
@@ -691,7 +696,10 @@ def _host_call(kernel, N, theta, phi, w, lanes, stops, trace, threads, step_hook
     corpus = _host_corpora.get(N, w)
     t1 = time.perf_counter()
     th = _upload_params(theta, lanes, "theta")
-    ph = _upload_params(phi.astype(theta.dtype, copy=False), lanes, "phi")
+    # float32 theta keeps a float64 phi as is (the reference's promotion);
+    # otherwise phi takes theta's dtype (float64 theta: exact widening)
+    keep64 = theta.dtype == np.float32 and phi.dtype == np.float64
+    ph = _upload_params(phi if keep64 else phi.astype(theta.dtype, copy=False), lanes, "phi")
     t2 = time.perf_counter()
     z = draw_z_device(kernel, corpus, th, ph, stops, lanes)  # synchronises (error check)
     t3 = time.perf_counter()
