@@ -79,12 +79,11 @@ class DeviceLDA:
         self.rank = self.torch.distributed.get_rank(process_group) if process_group is not None else 0
         self.shard_phi = (phi is None and world > 1 and self._phi_chunks % world == 0 and
                           os.environ.get("WD_SHARD_PHI", "1") != "0")
+        self._phi_bases = {}  # phi view data_ptr -> its padded base buffer (sharded resample)
         if self.shard_phi:
             rows_per = -(-self.V // self._phi_chunks)
             self._phi_rows_pad = rows_per * self._phi_chunks
-            base_view = block_aligned_rows(self._phi_rows_pad, self.K, self.dtype, dev, lanes)
-            self._phi_base = base_view._base if base_view._base is not None else base_view
-            self.phi = base_view[: self.V]
+            self.phi = self._alloc_phi()
             self._phi_part = torch.empty((self._phi_chunks, self.K), dtype=torch.float32, device=dev)
             self._phi_colstat = torch.empty(2 * self.K, dtype=torch.float32, device=dev)
         else:
@@ -126,6 +125,18 @@ class DeviceLDA:
         self._reducer = None  # in-flight per-tile count all-reduces (draw -> resample)
         n_err = self.tiles.n_tiles if self.tiles is not None else 1
         self.err = torch.empty((n_err, 2), dtype=torch.int64, device=dev)
+
+    def _alloc_phi(self):
+        """A [V, K] phi in the block_aligned_rows layout; with the sharded
+        resample, a view of a [chunks x rows_per, ld] buffer whose rank
+        slices are contiguous (registered for the rows' all-gather)."""
+        if not self.shard_phi:
+            return block_aligned_rows(self.V, self.K, self.dtype, self.device, self.lanes)
+        view = block_aligned_rows(self._phi_rows_pad, self.K, self.dtype, self.device, self.lanes)
+        base = view._base if view._base is not None else view
+        phi = view[: self.V]
+        self._phi_bases[phi.data_ptr()] = base
+        return phi
 
     # ------------------------------------------------------------ init
     def init_uniform(self, low: float = 0.1, high: float = 1.0, seed: int | None = None):
@@ -235,7 +246,7 @@ class DeviceLDA:
                 self._all_gather_slices(self._phi_part)
                 _lib.check(L.wd_resample_phi_reduce(pss, self._phi_part.data_ptr(), G, self.K,
                                                     self._phi_colstat.data_ptr(), st), "wd_resample_phi_reduce")
-        work = self._all_gather_slices(self._phi_base, async_op=True)
+        work = self._all_gather_slices(self._phi_bases[self.phi.data_ptr()], async_op=True)
         self._resample_theta(t)
         work.wait()
 
@@ -260,7 +271,7 @@ class DeviceLDA:
         if getattr(self, "_host_pipe", None) is None:
             self._host_pipe = {
                 "theta": [self.theta, block_aligned_rows(*self.theta.shape, self.theta.dtype, self.device, self.lanes)],
-                "phi": [self.phi, block_aligned_rows(*self.phi.shape, self.phi.dtype, self.device, self.lanes)],
+                "phi": [self.phi, self._alloc_phi()],
                 "z": [self.z, torch.empty_like(self.z)],
                 "z16": [None, None],
                 "up": torch.cuda.Stream(), "down": torch.cuda.Stream(),

@@ -33,7 +33,7 @@ def _problem():
     return M, V, K, N, off, words
 
 
-def _run(rank, world, port, out_dir, iters):
+def _run(rank, world, port, out_dir, iters, host=False):
     import paper_1505_03851_b200 as wd
     from paper_1505_03851_b200.device_lda import DeviceLDA
     from paper_1505_03851_b200.sharding import shard_csr, shard_ranges
@@ -51,11 +51,17 @@ def _run(rank, world, port, out_dir, iters):
     dc = wd.DeviceCorpus.from_csr(soff, swords, doc_base=lo)
     lda = DeviceLDA(dc, K, V, seed=5, process_group=pg, vocab_tile_bytes=64 * K * 4)
     lda.init_from_assignments()
-    for t in range(iters):
-        lda.iterate(t)
+    if host:  # parameters entering from pinned host memory each iteration
+        th_h = lda.theta.cpu().pin_memory()
+        ph_h = lda.phi.cpu().pin_memory()
+        lda.iterate_from_host(0, iters, th_h, ph_h)
+        torch.cuda.synchronize()
+    else:
+        for t in range(iters):
+            lda.iterate(t)
     lda.check_errors()
     ll = lda.log_likelihood()
-    np.savez(os.path.join(out_dir, f"r{world}_{rank}.npz"), z=lda.z.cpu().numpy(), theta=lda.theta.cpu().numpy(),
+    np.savez(os.path.join(out_dir, f"{'h' if host else 'r'}{world}_{rank}.npz"), z=lda.z.cpu().numpy(), theta=lda.theta.cpu().numpy(),
              phi=lda.phi.cpu().numpy(), wt=lda.word_topic.cpu().numpy(), ll=np.array(ll),
              sharded=np.array(lda.shard_phi))
     if world > 1:
@@ -80,6 +86,20 @@ def test_ranks_reproduce_one(tmp_path, world):
         np.testing.assert_array_equal(p["wt"], one["wt"])
         np.testing.assert_array_equal(p["phi"], one["phi"])
         assert abs(float(p["ll"]) - float(one["ll"])) <= 1e-9 * abs(float(one["ll"]))
+
+
+def test_two_ranks_reproduce_one_from_host(tmp_path):
+    """iterate_from_host (double-buffered theta / phi uploads) with the
+    sharded phi resample: 2 ranks equal 1 rank."""
+    iters = 2
+    _run(0, 1, 0, str(tmp_path), iters, True)
+    mp.start_processes(_run, args=(2, _free_port(), str(tmp_path), iters, True), nprocs=2, join=True,
+                       start_method="spawn")
+    one = np.load(tmp_path / "h1_0.npz")
+    parts = [np.load(tmp_path / f"h2_{r}.npz") for r in range(2)]
+    np.testing.assert_array_equal(np.concatenate([p["z"] for p in parts]), one["z"])
+    for p in parts:
+        np.testing.assert_array_equal(p["phi"], one["phi"])
 
 
 def test_bench_nccl_path_world1():
