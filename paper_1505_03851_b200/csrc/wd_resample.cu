@@ -80,6 +80,75 @@ __device__ __forceinline__ bool log_gamma_attempt(float a, const GammaRow& g, ui
   return false;
 }
 
+// Shapes below kSmallShape (the zero-count cells of theta: alpha = 0.1):
+// the small-shape sampler of Liu, Martin & Syring (2017), exact, one
+// Philox block per attempt, no normal variate.  Z = -a log X has density
+// proportional to exp(-z - e^(-z/a)); the envelope is e^(-z) on z >= 0 (mass 1)
+// and e^(lambda z - 1) on z < 0 (mass w), lambda = 1/a - 1, w = a / (e (1 - a)).
+// In y = -z/a = log X:
+//   with probability 1/(1+w): y = log(U (1+w)) / a  (y <= 0), accepted when log V < -e^y;
+//   otherwise:                y = -log(U') / (1 - a) (y > 0), accepted when log V < 1 + y - e^y.
+// Acceptance at a = 0.1: Gamma(1.1) / (1 + w) = 0.91.
+constexpr float kSmallShape = 0.5f;
+__device__ __forceinline__ bool log_gamma_small_attempt(float a, const GammaRow& g, uint32_t k, uint32_t ctr,
+                                                        float& out) {
+  const uint4 r = rand4(g, k, ctr);
+  const float w = __fdividef(a, 2.718281828459045f * (1.f - a));
+  const float one_w = 1.f + w;
+  const float u = u01(r.x);
+  float y;
+  if (u * one_w <= 1.f) y = __fdividef(__logf(u * one_w), a);
+  else y = __fdividef(-__logf(u01(r.y)), 1.f - a);
+  const float ey = __expf(y);
+  const float lv = __logf(u01(r.z));
+  if (y <= 0.f ? lv < -ey : lv < 1.f + y - ey) {
+    out = y;
+    return true;
+  }
+  return false;
+}
+// one attempt for any shape (the per-cell entry point of wd_log_gamma_draws)
+__device__ __forceinline__ bool log_gamma_any(float a, const GammaRow& g, uint32_t k, uint32_t ctr, float& out) {
+  return a < kSmallShape ? log_gamma_small_attempt(a, g, k, ctr, out) : log_gamma_attempt(a, g, k, ctr, out);
+}
+
+// Warp-level queue of the cells of one document that need the general
+// (Marsaglia-Tsang) sampler: shape >= kSmallShape, i.e. the topics the
+// document's tokens hit (need_of(k), evaluated by lane k mod 32).  They are a minority (e.g. ~17% at K = 1024 with
+// 200 tokens); gathering them 32 at a time keeps every lane busy on one.
+template <typename Need, typename Shape, typename Store>
+__device__ __forceinline__ void warp_general_cells(int K, int lane, int* q, const GammaRow& rkey, Need need_of,
+                                                   Shape shape, Store store) {
+  int qn = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  auto drain = [&](int n) {  // lanes < n take q[lane]
+    if (lane < n) {
+      const int k = q[lane];
+      const float a = shape(k);
+      float v;
+      uint32_t ctr = 0;
+      while (!log_gamma_attempt(a, rkey, (uint32_t)k, ctr, v)) ++ctr;
+      store(k, v);
+    }
+    __syncwarp();
+  };
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    const int k = k0 + lane;
+    const bool need = k < K && need_of(k);  // evaluated by the lane that owns topic k
+    const unsigned m = __ballot_sync(FULL, need);
+    if (need) q[qn + __popc(m & lt)] = k;
+    qn += __popc(m);
+    __syncwarp();
+    if (qn >= 32) {
+      drain(32);
+      if (lane < qn - 32) q[lane] = q[32 + lane];
+      __syncwarp();
+      qn -= 32;
+    }
+  }
+  drain(qn);
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
@@ -116,10 +185,13 @@ __global__ void __launch_bounds__(256) theta_kernel(const int32_t* __restrict__ 
     __syncwarp();
     const uint64_t row = (uint64_t)(doc_base + m);
     float mx = -INFINITY;
-    // per-lane progress: a rejection costs that lane one more attempt instead
-    // of stalling the whole warp at every topic (divergence only at the tail)
-    uint32_t ctr = 0;
     const GammaRow rkey = gamma_row(seed, row);
+    // per-lane progress: a rejection costs that lane one more attempt instead
+    // of stalling the whole warp at every topic (divergence only at the
+    // tail).  (The two-phase small-shape + queued general sampling of the
+    // wide kernel measured slower here: K = 200 / 1024 / 2048 resample
+    // 1.67 / 4.37 / 12.6 -> 2.26 / 5.88 / 14.0 ms.)
+    uint32_t ctr = 0;
     for (int k = lane; k < K;) {
       float v;
       if (log_gamma_attempt(alpha + (float)hist[k], rkey, (uint32_t)k, ctr, v)) {
@@ -151,8 +223,12 @@ __global__ void __launch_bounds__(256) theta_kernel(const int32_t* __restrict__ 
 // log-Gammas go to the document's output row, normalised there in two more
 // coalesced passes.  4 B/topic of shared memory per warp became 2 B/topic:
 // at K = 4096 the plain kernel fit 8 warps per SM and was latency-bound.
-// Used above K = 2048.
-// Bit-identical to theta_kernel (same attempts, same per-lane order).
+// Used above K = 2048.  Sampling in two phases: the topics the document's
+// tokens did not hit (shape alpha < 1/2) with the small-shape sampler,
+// per-lane progress, then the hit topics gathered 32 at a time for
+// Marsaglia-Tsang (warp_general_cells): configs[4] shard resample 45.2 ->
+// 41.1 ms (at K <= 2048 the same scheme was slower; theta_kernel keeps the
+// single loop).
 __global__ void __launch_bounds__(256) theta_kernel_wide(const int32_t* __restrict__ z,
                                                          const int64_t* __restrict__ off, int64_t n_docs, int32_t K,
                                                          float alpha, uint64_t seed, int64_t doc_base,
@@ -161,7 +237,8 @@ __global__ void __launch_bounds__(256) theta_kernel_wide(const int32_t* __restri
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int KW = (K + 1) >> 1;
-  uint32_t* h2 = hsm + (size_t)wib * KW;
+  uint32_t* h2 = hsm + (size_t)wib * (KW + 64);
+  int* q = reinterpret_cast<int*>(h2 + KW);  // the general-sampler queue (64)
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t m = (int64_t)blockIdx.x * wpb + wib; m < n_docs; m += (int64_t)gridDim.x * wpb) {
     float* out = theta + m * ld;
@@ -186,18 +263,43 @@ __global__ void __launch_bounds__(256) theta_kernel_wide(const int32_t* __restri
     __syncwarp();
     const GammaRow rkey = gamma_row(seed, (uint64_t)(doc_base + m));
     float mx = -INFINITY;
-    uint32_t ctr = 0;
-    for (int k = lane; k < K;) {
-      const int cnt = big ? __ldcg(gh + k) : (int)((h2[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu);
-      float v;
-      if (log_gamma_attempt(alpha + (float)cnt, rkey, (uint32_t)k, ctr, v)) {
-        out[k] = v;  // (a big document's count at k is read above, then replaced)
-        mx = fmaxf(mx, v);
-        k += 32;
-        ctr = 0;
-      } else {
-        ++ctr;
+    if (big) {  // counts in the output row itself: one pass, one sampler per cell
+      uint32_t ctr = 0;
+      for (int k = lane; k < K;) {
+        const int cnt = __ldcg(gh + k);
+        float v;
+        if (log_gamma_any(alpha + (float)cnt, rkey, (uint32_t)k, ctr, v)) {
+          out[k] = v;  // (the count at k is read above, then replaced)
+          mx = fmaxf(mx, v);
+          k += 32;
+          ctr = 0;
+        } else {
+          ++ctr;
+        }
       }
+    } else {
+      auto shape = [&](int k) { return alpha + (float)((h2[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu); };
+      uint32_t ctr = 0;
+      for (int k = lane; k < K;) {  // (1) small shapes, per-lane progress
+        const float a = shape(k);
+        if (!(a < kSmallShape)) {
+          k += 32;
+          continue;
+        }
+        float v;
+        if (log_gamma_small_attempt(a, rkey, (uint32_t)k, ctr, v)) {
+          out[k] = v;
+          mx = fmaxf(mx, v);
+          k += 32;
+          ctr = 0;
+        } else {
+          ++ctr;
+        }
+      }
+      __syncwarp();
+      // (2) the rest, 32 at a time
+      warp_general_cells(K, lane, q, rkey, [&](int k) { return !(shape(k) < kSmallShape); }, shape,
+                         [&](int k, float v) { out[k] = v; mx = fmaxf(mx, v); });
     }
     mx = warp_max(mx);
     float sum = 0.f;
@@ -220,7 +322,7 @@ __global__ void log_gamma_cells(uint64_t seed, const int64_t* __restrict__ rows,
     const GammaRow g = gamma_row(seed, (uint64_t)rows[i]);
     float v;
     uint32_t ctr = 0;
-    while (!log_gamma_attempt(shapes[i], g, (uint32_t)topics[i], ctr, v)) ++ctr;
+    while (!log_gamma_any(shapes[i], g, (uint32_t)topics[i], ctr, v)) ++ctr;
     out[i] = v;
   }
 }
@@ -354,7 +456,7 @@ static int resample_theta_t(const int32_t* z, const int64_t* off, int64_t n_docs
   const int threads = 256;
   if constexpr (std::is_same<T, float>::value) {
     if (K > 2048) {  // measured (1M docs): K = 4096 44.4 -> 31.1 ms; K = 2048 10.7 -> 12.2 (kept plain)
-      const size_t smem_w = (size_t)(threads / 32) * ((K + 1) / 2) * sizeof(uint32_t);
+      const size_t smem_w = (size_t)(threads / 32) * ((K + 1) / 2 + 64) * sizeof(uint32_t);
       if (smem_w > 48 * 1024)
         cudaFuncSetAttribute((const void*)theta_kernel_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem_w);
