@@ -21,6 +21,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "warpdraw_b200.h"
@@ -455,7 +456,13 @@ static int resample_theta_t(const int32_t* z, const int64_t* off, int64_t n_docs
                             int64_t doc_base, T* theta, int64_t ld, cudaStream_t st) {
   const int threads = 256;
   if constexpr (std::is_same<T, float>::value) {
-    if (K > 2048) {  // measured (1M docs): K = 4096 44.4 -> 31.1 ms; K = 2048 10.7 -> 12.2 (kept plain)
+    // measured (1M docs): K = 4096 44.4 -> 31.1 ms; K = 2048 10.7 -> 12.2 (kept plain);
+    // WD_THETA_WIDE_MIN_K overrides the threshold (A/B)
+    static const int wide_min = [] {
+      const char* e = getenv("WD_THETA_WIDE_MIN_K");
+      return (e && e[0]) ? atoi(e) : 2049;
+    }();
+    if (K >= wide_min) {
       const size_t smem_w = (size_t)(threads / 32) * ((K + 1) / 2 + 64) * sizeof(uint32_t);
       if (smem_w > 48 * 1024)
         cudaFuncSetAttribute((const void*)theta_kernel_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
