@@ -114,22 +114,28 @@ def main():
     ap.add_argument("--vocab", type=int, default=40_000)
     ap.add_argument("--mean-len", type=float, default=200.0)
     ap.add_argument("--seed", type=int, default=2026)
+    ap.add_argument("--only-n", type=int, default=None,
+                    help="model this world size only (e.g. configs[4]: --docs 10000000 --topics 4096 --only-n 8)")
+    ap.add_argument("--all-ranks", action="store_true", help="time every rank's shard (default: first and last)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     res = {"assumption": f"ring all-reduce busbw {args.busbw_gbs} GB/s (NVLink 5); only the last vocabulary tile's "
                          "count all-reduce is exposed", "per_n": {}}
     t1 = None
-    for N in (1, 2, 4, 8):
-        ranks = sorted({0, N - 1})
+    total_tokens = None
+    for N in ((args.only_n,) if args.only_n else (1, 2, 4, 8)):
+        ranks = list(range(N)) if args.all_ranks else sorted({0, N - 1})
         shards = [time_shard(args, r, N, dev) for r in ranks]
+        if args.all_ranks:
+            total_tokens = sum(x["tokens"] for x in shards)
         worst = max(shards, key=lambda s: s["iter_ms"])
         tile_bytes = worst["rows_per_tile"] * args.topics * 4
         ar_ms = 0.0 if N == 1 else 2 * (N - 1) / N * tile_bytes / (args.busbw_gbs * 1e9) * 1e3
         t_n = worst["iter_ms"] + ar_ms
         if N == 1:
             t1 = t_n
-        if N == 1:
             total_tokens = shards[0]["tokens"]
+        eff = (lambda t: t1 / (N * t)) if t1 else (lambda t: None)
         # sharded phi (DeviceLDA default for N > 1): the rank's phi share, two
         # column-partial all-gathers (~latency), then the rows' all-gather
         # overlapping the theta resample
@@ -139,11 +145,13 @@ def main():
                 if N > 1 else t_n)
         res["per_n"][N] = {"shards": shards, "exposed_allreduce_ms": ar_ms,
                            "replicated_phi": {"predicted_iter_ms": t_n, "predicted_tokens_per_s": total_tokens / (t_n / 1e3),
-                                              "predicted_efficiency": t1 / (N * t_n)},
+                                              "predicted_efficiency": eff(t_n)},
                            "sharded_phi": {"phi_allgather_ms": ag_ms, "partials_allgather_ms": part_ms,
                                            "predicted_iter_ms": t_sh,
                                            "predicted_tokens_per_s": total_tokens / (t_sh / 1e3),
-                                           "predicted_efficiency": t1 / (N * t_sh)}}
+                                           "predicted_efficiency": eff(t_sh)}}
+        if args.all_ranks:
+            res["per_n"][N]["sum_of_shard_iterations_ms"] = sum(x["iter_ms"] for x in shards)
     print(json.dumps(res))
 
 
