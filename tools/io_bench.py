@@ -40,7 +40,7 @@ def main():
     out["file_bytes"] = os.path.getsize(path)
     torch.cuda.init()
     torch.empty(1, device="cuda")
-    for label, kw in (("whole", {}), ("rank0_of_8", {"rank": 0, "world": 8})):
+    for label, kw in (("whole_first_call", {}), ("whole", {}), ("rank0_of_8", {"rank": 0, "world": 8})):
         tim = {}
         dc = C.load_device_corpus(path, timing=tim, **kw)
         out[label] = {"docs": dc.n_docs, "tokens": dc.n_tokens, **{k: round(v, 3) for k, v in tim.items()}}
