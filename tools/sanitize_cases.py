@@ -35,6 +35,53 @@ for K, W, dt in ((200, 32, np.float32), (64, 8, np.float64), (128, 32, np.float3
         wd.draw_z_device(kern, dc, th, ph, wd.SeededStops(3), W)
         wd.draw_z_device(kern, dc, th, ph, wd.SeededStops(3), W, tiles=tiles)
         wd.draw_z_device(kern, dc, tha, pha, wd.SeededStops(3), W, tiles=tiles_p)
+# round 2: one-row-per-thread rows (K < 32, remnant shapes)
+for K in (8, 16, 24, 40, 136):
+    w = torch.from_numpy(gen.uniform(0.1, 1, size=(300, K)).astype(np.float32)).cuda()
+    wd.sample_rows(w, 2, lanes=32)
+# round 2: small-K and register-lean LDA kernels on run-padded and unpadded tiles
+for K in (64, 200, 232, 2048, 4096):
+    M, V = 96, 120
+    N = gen.poisson(15, size=M)
+    off = np.concatenate([[0], np.cumsum(N)])
+    words = gen.integers(0, V, size=int(off[-1])).astype(np.int32)
+    dc = wd.DeviceCorpus.from_csr(off, words)
+    tha = wd.kernels.to_block_aligned(torch.from_numpy(gen.uniform(0.1, 1, size=(M, K)).astype(np.float32)).cuda())
+    pha = wd.kernels.to_block_aligned(torch.from_numpy(gen.uniform(0.1, 1, size=(V, K)).astype(np.float32)).cuda())
+    wt = torch.zeros((V, K), dtype=torch.int32, device="cuda")
+    for pad in (0, 4):
+        wd.draw_z_device("butterfly", dc, tha, pha, wd.SeededStops(4), 32, tiles=dc.vocab_tiles(40, pad),
+                         word_topic=wt)
+    # float32 theta with float64 phi (wd_mixed.cu), all three kernels
+    ph64 = torch.from_numpy(gen.uniform(0.1, 1, size=(V, K))).cuda()
+    for kern in ("butterfly", "transposed", "basic"):
+        wd.draw_z_device(kern, dc, tha, ph64, wd.SeededStops(4), 32)
+# round 2: the split table / search API
+for W, K in ((8, 21), (64, 150), (32, 32)):
+    prods = gen.uniform(0.0, 1.0, size=(5, W, K)).astype(np.float32)
+    warp, p, sums = wd.build_block_tables(prods, wd.WarpConfig(lanes=W))
+    wd.butterfly_search(warp, p, sums, (sums * 0.5).astype(np.float32))
+# round 2: sharded phi passes (a rank's chunk range) and the wide theta kernel
+from paper_1505_03851_b200 import _lib  # noqa: E402
+
+L = _lib.load()
+V, K = 300, 96
+wt = torch.randint(0, 5, (V, K), dtype=torch.int32, device="cuda")
+phi = torch.empty((V, K), device="cuda")
+G = int(L.wd_resample_phi_chunks())
+part = torch.empty((G, K), device="cuda")
+col = torch.zeros(2 * K, device="cuda")
+for pss in (0, 1, 2):
+    _lib.check(L.wd_resample_phi_pass(0, pss, wt.data_ptr(), V, K, 0.01, 7, phi.data_ptr(), K, G // 4, G // 2, G,
+                                      part.data_ptr(), col.data_ptr(), _lib.stream_handle()), "pass")
+    if pss < 2:
+        _lib.check(L.wd_resample_phi_reduce(pss, part.data_ptr(), G, K, col.data_ptr(), _lib.stream_handle()), "red")
+M, V, K = 64, 60, 2112
+off = np.concatenate([[0], np.cumsum(gen.poisson(30, size=M))])
+words = gen.integers(0, V, size=int(off[-1])).astype(np.int32)
+lda = DeviceLDA(wd.DeviceCorpus.from_csr(off, words), K, V, seed=1)
+lda.init_from_assignments()
+lda.iterate(0)
 # device LDA iteration (counts, resample, log-likelihood)
 M, V, K = 64, 50, 48
 off = np.concatenate([[0], np.cumsum(gen.poisson(20, size=M))])
