@@ -34,6 +34,9 @@
 
 namespace wd {
 
+#ifndef WD_SMALL_GROUP  // blocks whose loads may be in flight together (the opaque dependency every GROUP blocks)
+#define WD_SMALL_GROUP 1
+#endif
 #ifndef WD_SMALL_EARLY
 #define WD_SMALL_EARLY 0  // measured at K = 200: 14.8 vs 13.6 ms (register pressure)
 #endif
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(128, WD_SMALL_LDA_MIN_BLOCKS) lda_small_kernel
       // block b's loads depend on block b-1's sum through an opaque runtime
       // zero: one block in flight per warp, so the unrolled loop keeps the
       // register budget of one block
-      const int64_t col = (int64_t)b * W + (int64_t)(__float_as_uint(acc) & p.opaque_zero);
+      const int64_t col = (int64_t)b * W + ((b % WD_SMALL_GROUP) == 0 ? (int64_t)(__float_as_uint(acc) & p.opaque_zero) : 0);
       float q[L];
       if (fast) {
         // all five loads of the block in flight together: every consumer
