@@ -208,8 +208,10 @@ class DeviceLDA:
         flat = buf.view(-1)
         n = flat.numel() // self.world
         mine = flat[self.rank * n:(self.rank + 1) * n]
+        # the rank's slice is sent from a copy (1/world of the buffer): no
+        # reliance on in-place semantics of the collective
         if dist.get_backend(self.pg) == "nccl":
-            return dist.all_gather_into_tensor(flat, mine, group=self.pg, async_op=async_op)
+            return dist.all_gather_into_tensor(flat, mine.clone(), group=self.pg, async_op=async_op)
         return dist.all_gather(list(flat.split(n)), mine.clone(), group=self.pg, async_op=async_op)
 
     def resample(self, t: int):
