@@ -667,16 +667,19 @@ def main():
         out = torch.empty(n, dtype=torch.int32, device=dev)
         err = torch.empty(2, dtype=torch.int64, device=dev)
         for var in ("butterfly", "prefix"):
+            err.fill_(-1)  # one reset for the batch of draws (WD_ERR_ACCUMULATE), checked after
             for _ in range(3):
-                wd.sample_rows(wts, 5, variant=var, out=out, err=err, check=False)
+                wd.sample_rows(wts, 5, variant=var, out=out, err=err, check=False, accumulate_err=True)
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             for _ in range(10):
-                wd.sample_rows(wts, 5, variant=var, out=out, err=err, check=False)
+                wd.sample_rows(wts, 5, variant=var, out=out, err=err, check=False, accumulate_err=True)
             b.record(stream)
             torch.cuda.synchronize()
             res[var] = a.elapsed_time(b) / 1e3 / 10
+            if int(err.cpu().numpy().view(np.uint64)[0]) != (1 << 64) - 1:
+                raise RuntimeError("a sampler row summed to zero")
         bpd = 4 * K + 4
         sampler = {
             "workload": f"standalone rows n={n} K={K} fp32 W=32 (configs[1]), weights 4.3 GB > L2",

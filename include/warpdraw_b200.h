@@ -149,6 +149,18 @@ int wd_sample_rows(int variant, int dtype, int lanes, const void* weights, int64
                    int64_t n_rows, int32_t n_topics, int64_t row_base, int stop_mode,
                    uint64_t seed, const double* units, const void* stops, int32_t* out,
                    uint64_t* err, void* workspace, size_t workspace_bytes, void* stream);
+/*
+ * wd_sample_rows with flags.  WD_ERR_ACCUMULATE: err is NOT reset to
+ * all-ones first -- errors of consecutive calls accumulate (min key, and of
+ * the range flags) until the caller resets the two words itself (one
+ * memset for a batch of draws; a per-call reset is a separate stream
+ * operation, ~4-5 us, as long as a 2^20-row draw at K <= 32).
+ */
+#define WD_ERR_ACCUMULATE 1
+int wd_sample_rows_ex(int variant, int dtype, int lanes, const void* weights, int64_t ld,
+                      int64_t n_rows, int32_t n_topics, int64_t row_base, int stop_mode,
+                      uint64_t seed, const double* units, const void* stops, int32_t* out,
+                      uint64_t* err, void* workspace, size_t workspace_bytes, int flags, void* stream);
 
 /* units_for(seed, k0[i][, k1[i]]) for n_keys in {0,1,2} (rng.py:101-122). */
 int wd_units(uint64_t seed, int n_keys, const int64_t* k0, const int64_t* k1, int64_t n,

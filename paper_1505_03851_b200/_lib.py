@@ -22,6 +22,7 @@ WD_STOPS_SEEDED, WD_STOPS_UNITS, WD_STOPS_EXPLICIT, WD_STOPS_PHILOX = 0, 1, 2, 3
 WD_KEYS_MASTER, WD_KEYS_POSITION = 0, 1
 WD_STREAM_BINARY, WD_STREAM_ALIAS = 0, 1
 ERR_NONE = (1 << 64) - 1
+WD_ERR_ACCUMULATE = 1
 
 EXPORTS = (
     "wd_abi_version",
@@ -45,6 +46,7 @@ EXPORTS = (
     "wd_l2_read_probe",
     "wd_build_block_tables",
     "wd_butterfly_search",
+    "wd_sample_rows_ex",
     "wd_resample_phi_chunks",
     "wd_resample_phi_pass",
     "wd_resample_phi_reduce",
@@ -77,6 +79,9 @@ def _declare(L):
     L.wd_sample_rows.restype = i32
     L.wd_sample_rows.argtypes = [i32, i32, i32, vp, i64, i64, ctypes.c_int32, i64, i32, u64, vp, vp, vp, vp, vp,
                                  sz, vp]
+    L.wd_sample_rows_ex.restype = i32
+    L.wd_sample_rows_ex.argtypes = [i32, i32, i32, vp, i64, i64, ctypes.c_int32, i64, i32, u64, vp, vp, vp, vp, vp,
+                                    sz, i32, vp]
     L.wd_units.restype = i32
     L.wd_units.argtypes = [u64, i32, vp, vp, i64, vp, vp]
     L.wd_topic_counts.restype = i32

@@ -261,6 +261,14 @@ int wd_sample_rows(int variant, int dtype, int lanes, const void* weights, int64
                    int32_t n_topics, int64_t row_base, int stop_mode, uint64_t seed, const double* units,
                    const void* stops, int32_t* out, uint64_t* err, void* workspace, size_t workspace_bytes,
                    void* stream) {
+  return wd_sample_rows_ex(variant, dtype, lanes, weights, ld, n_rows, n_topics, row_base, stop_mode, seed, units,
+                           stops, out, err, workspace, workspace_bytes, 0, stream);
+}
+
+int wd_sample_rows_ex(int variant, int dtype, int lanes, const void* weights, int64_t ld, int64_t n_rows,
+                      int32_t n_topics, int64_t row_base, int stop_mode, uint64_t seed, const double* units,
+                      const void* stops, int32_t* out, uint64_t* err, void* workspace, size_t workspace_bytes,
+                      int flags, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (!valid_lanes(lanes) || (dtype != WD_FLOAT32 && dtype != WD_FLOAT64) || n_topics <= 0 || n_rows < 0 ||
       ld < 0 || (variant != WD_BUTTERFLY && variant != WD_PREFIX))
@@ -268,7 +276,8 @@ int wd_sample_rows(int variant, int dtype, int lanes, const void* weights, int64
   if (stop_mode < WD_STOPS_SEEDED || stop_mode > WD_STOPS_PHILOX) return WD_ERR_INVALID_ARGUMENT;
   if (stop_mode == WD_STOPS_UNITS && !units) return WD_ERR_INVALID_ARGUMENT;
   if (stop_mode == WD_STOPS_EXPLICIT && !stops) return WD_ERR_INVALID_ARGUMENT;
-  int rc = reset_err(err, st);
+  if (!err) return WD_ERR_INVALID_ARGUMENT;
+  int rc = (flags & WD_ERR_ACCUMULATE) ? WD_OK : reset_err(err, st);
   if (rc != WD_OK) return rc;
   if (n_rows == 0) return WD_OK;
   if (!weights || !out) return WD_ERR_INVALID_ARGUMENT;

@@ -40,7 +40,7 @@ def _dtype_code(t):
 
 def sample_rows(weights, seed: int | None = None, *, lanes: int = 32, variant: str = "butterfly", row_base: int = 0,
                 units=None, stops=None, out=None, n: int | None = None, err=None, check: bool = True, stream=None,
-                raw_seed: int | None = None):
+                raw_seed: int | None = None, accumulate_err: bool = False):
     """Draw one index per row of `weights` ([n, K] CUDA tensor, float32/64).
 
     A 1-D weights tensor is one shared vector; pass n for the number of draws.
@@ -48,6 +48,9 @@ def sample_rows(weights, seed: int | None = None, *, lanes: int = 32, variant: s
     `units` (float64 per row) or `stops` (explicit, weights dtype) are given.
     Returns an int32 CUDA tensor.  Rows summing to zero raise AllZeroError
     when check=True (the reference's search returns index K-1 for them).
+    accumulate_err=True (with a caller-owned err and check=False): err is not
+    reset first, so a batch of calls shares one reset and one check
+    (WD_ERR_ACCUMULATE) instead of a reset per call.
     """
     import torch
 
@@ -83,9 +86,12 @@ def sample_rows(weights, seed: int | None = None, *, lanes: int = 32, variant: s
     L = _lib.load()
     v = _VARIANTS[variant]
     ws, nbytes = _workspace(v, dt, int(lanes), K, dev)
-    _lib.check(L.wd_sample_rows(v, dt, int(lanes), weights.data_ptr(), ld, n, K, int(row_base), mode,
-                                int(sd) & ((1 << 64) - 1), _lib.ptr(u_t), _lib.ptr(s_t), out.data_ptr(),
-                                err.data_ptr(), _lib.ptr(ws), nbytes, _lib.stream_handle(stream)),
+    if accumulate_err and (own_err or check):
+        raise ValueError("accumulate_err needs a caller-owned err and check=False")
+    _lib.check(L.wd_sample_rows_ex(v, dt, int(lanes), weights.data_ptr(), ld, n, K, int(row_base), mode,
+                                   int(sd) & ((1 << 64) - 1), _lib.ptr(u_t), _lib.ptr(s_t), out.data_ptr(),
+                                   err.data_ptr(), _lib.ptr(ws), nbytes,
+                                   _lib.WD_ERR_ACCUMULATE if accumulate_err else 0, _lib.stream_handle(stream)),
                "wd_sample_rows")
     if check:
         e = err.cpu().numpy().view(np.uint64)

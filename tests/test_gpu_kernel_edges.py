@@ -76,3 +76,23 @@ def test_injected_philox_and_doc_base(K):
     z_u = wd.draw_z_device("butterfly", dc, th, ph, torch.from_numpy(wd.rng.philox_units(seed, doc, pos)).cuda(), 32,
                            tiles=tiles).cpu().numpy()
     np.testing.assert_array_equal(z_p, z_u)
+
+
+def test_sampler_error_accumulation():
+    """WD_ERR_ACCUMULATE: one caller-owned err over a batch of draws keeps the
+    first batch's AllZero row; a normal call resets it."""
+    gen = np.random.default_rng(5)
+    for K in (16, 1024):
+        w = torch.from_numpy(gen.uniform(0.1, 1, size=(300, K)).astype(np.float32)).cuda()
+        wz = w.clone()
+        wz[123] = 0
+        err = torch.empty(2, dtype=torch.int64, device="cuda")
+        err.fill_(-1)
+        wd.sample_rows(wz, 1, err=err, check=False, accumulate_err=True)
+        wd.sample_rows(w, 2, err=err, check=False, accumulate_err=True)
+        e = err.cpu().numpy().view(np.uint64)
+        assert int(e[0]) == 123 and int(e[1]) == (1 << 64) - 1
+        wd.sample_rows(w, 3, err=err, check=False)  # resets first
+        assert int(err.cpu().numpy().view(np.uint64)[0]) == (1 << 64) - 1
+        with pytest.raises(ValueError, match="caller-owned err"):
+            wd.sample_rows(w, 3, accumulate_err=True)

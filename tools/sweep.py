@@ -20,6 +20,7 @@ import json
 import os
 import sys
 
+import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -85,7 +86,14 @@ def main():
         fl = flush if n * K * 4 < (512 << 20) else None
         r = {"K": K}
         for var in ("butterfly", "prefix"):
-            dt = timed(lambda: wd.sample_rows(w, 5, variant=var, out=out, err=err, check=False), fl)
+            # errors accumulate over the timed calls (one reset, checked after):
+            # the per-call reset is a separate stream operation as long as a
+            # small-K draw (WD_ERR_ACCUMULATE)
+            err.fill_(-1)
+            dt = timed(lambda: wd.sample_rows(w, 5, variant=var, out=out, err=err, check=False,
+                                              accumulate_err=True), fl)
+            if err.cpu().numpy().view(np.uint64)[0] != np.uint64(2**64 - 1):
+                raise RuntimeError("a sweep row summed to zero")
             r[var] = {"ms": dt * 1e3, "draws_per_s": n / dt, "frac": n * (4 * K + 4) / dt / 1e9 / peak}
         r["speedup"] = r["prefix"]["ms"] / r["butterfly"]["ms"]
         rows.append(r)
