@@ -140,7 +140,17 @@ __device__ __forceinline__ void lane_row_draw(const DrawParams<float>& p, int64_
 // small enough; register-heavy shapes run 6 CTAs per SM instead of 8.
 template <int NB, int RM> struct LaneShape {
   static constexpr int FLOATS = NB * 32 + RM * 8;
-  static constexpr int RPT = FLOATS <= 8 ? 4 : (FLOATS <= 16 ? 2 : 1);
+#ifndef WD_ROWS_LANE_RPT32  // rows per thread for 17-32 floats (A/B)
+#define WD_ROWS_LANE_RPT32 1
+#endif
+#ifndef WD_ROWS_LANE_RPT8
+#define WD_ROWS_LANE_RPT8 4
+#endif
+#ifndef WD_ROWS_LANE_RPT16
+#define WD_ROWS_LANE_RPT16 2
+#endif
+  static constexpr int RPT = FLOATS <= 8 ? WD_ROWS_LANE_RPT8
+                                         : (FLOATS <= 16 ? WD_ROWS_LANE_RPT16 : (FLOATS <= 32 ? WD_ROWS_LANE_RPT32 : 1));
   static constexpr int MINB = FLOATS * RPT > 40 ? 6 : WD_ROWS_LANE_MIN_BLOCKS;
 };
 
