@@ -75,7 +75,7 @@ def build_host(force: bool = False) -> str:
     if cc is None:
         raise RuntimeError("no C compiler for the host helper")
     tmp = out + ".tmp"
-    cmd = [cc, "-O2", "-shared", "-fPIC", "-std=c11", "-Wall", f"-I{sysconfig.get_paths()['include']}",
+    cmd = [cc, "-O2", "-shared", "-fPIC", "-std=gnu11", "-Wall", "-pthread", f"-I{sysconfig.get_paths()['include']}",
            f"-I{np.get_include()}", HOST_SRC, "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -20,13 +20,22 @@
  *                                      then uses numpy), ValueError when a list
  *                                      is shorter than its length, OverflowError
  *                                      when an id does not fit int32.
+ *   widen_i32(addr, n, threads)     -> fresh int64 array of the n int32 at addr
+ *                                      (e.g. a pinned D2H buffer): an anonymous
+ *                                      mapping advised for transparent huge
+ *                                      pages, filled by `threads` threads
+ *                                      (the page faults of a fresh 1.6 GB
+ *                                      buffer cost more than the copy).
  */
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
 #define NPY_NO_DEPRECATED_API NPY_1_7_API_VERSION
 #include <numpy/arrayobject.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <string.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
 static PyObject* ragged_views(PyObject* self, PyObject* args) {
   PyArrayObject *z, *off;
@@ -203,11 +212,93 @@ static PyObject* concat_ragged(PyObject* self, PyObject* args) {
   return Py_BuildValue("(NLL)", out, (long long)lo, (long long)hi);
 }
 
+
+/* ---------------------------------------------------------------- widen */
+typedef struct {
+  const int32_t* src;
+  int64_t* dst;
+  npy_intp a, b;
+} widen_job;
+
+static void* widen_worker(void* arg) {
+  widen_job* j = (widen_job*)arg;
+  for (npy_intp i = j->a; i < j->b; ++i) j->dst[i] = j->src[i];
+  return NULL;
+}
+
+static void unmap_capsule(PyObject* cap) {
+  void* p = PyCapsule_GetPointer(cap, "wd_mmap");
+  size_t* sz = (size_t*)PyCapsule_GetContext(cap);
+  if (p && sz) munmap(p, *sz);
+  free(sz);
+}
+
+static PyObject* widen_i32(PyObject* self, PyObject* args) {
+  unsigned long long addr;
+  Py_ssize_t n;
+  int threads;
+  (void)self;
+  if (!PyArg_ParseTuple(args, "Kni", &addr, &n, &threads)) return NULL;
+  if (n < 0 || (n > 0 && addr == 0)) {
+    PyErr_SetString(PyExc_ValueError, "widen_i32: bad buffer");
+    return NULL;
+  }
+  const size_t bytes = (size_t)(n > 0 ? n : 1) * sizeof(int64_t);
+  const size_t huge = (size_t)2 << 20;
+  const size_t len = (bytes + huge - 1) / huge * huge;
+  void* mem = mmap(NULL, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (mem == MAP_FAILED) return PyErr_NoMemory();
+  madvise(mem, len, MADV_HUGEPAGE);
+  int T = threads < 1 ? 1 : (threads > 64 ? 64 : threads);
+  if (n < ((npy_intp)1 << 20)) T = 1;
+  pthread_t th[64];
+  widen_job jobs[64];
+  Py_BEGIN_ALLOW_THREADS;
+  for (int t = 0; t < T; ++t) {
+    jobs[t].src = (const int32_t*)(uintptr_t)addr;
+    jobs[t].dst = (int64_t*)mem;
+    jobs[t].a = (npy_intp)((int64_t)n * t / T);
+    jobs[t].b = (npy_intp)((int64_t)n * (t + 1) / T);
+    if (T > 1) pthread_create(&th[t], NULL, widen_worker, &jobs[t]);
+    else widen_worker(&jobs[t]);
+  }
+  if (T > 1)
+    for (int t = 0; t < T; ++t) pthread_join(th[t], NULL);
+  Py_END_ALLOW_THREADS;
+  npy_intp dims[1] = {n};
+  PyObject* arr = PyArray_SimpleNewFromData(1, dims, NPY_INT64, mem);
+  if (!arr) {
+    munmap(mem, len);
+    return NULL;
+  }
+  size_t* szp = (size_t*)malloc(sizeof(size_t));
+  if (!szp) {
+    Py_DECREF(arr);
+    munmap(mem, len);
+    return PyErr_NoMemory();
+  }
+  *szp = len;
+  PyObject* cap = PyCapsule_New(mem, "wd_mmap", unmap_capsule);
+  if (!cap) {
+    free(szp);
+    Py_DECREF(arr);
+    munmap(mem, len);
+    return NULL;
+  }
+  PyCapsule_SetContext(cap, szp);
+  if (PyArray_SetBaseObject((PyArrayObject*)arr, cap) < 0) {
+    Py_DECREF(arr);
+    return NULL;
+  }
+  return arr;
+}
+
 static PyMethodDef methods[] = {
     {"ragged_views", ragged_views, METH_VARARGS, "list of views z[offsets[m]:offsets[m+1]]"},
     {"list_ids", list_ids, METH_O, "int64 ids of the list's elements"},
     {"ids_equal", ids_equal, METH_VARARGS, "same list elements (by identity)"},
     {"concat_ragged", concat_ragged, METH_VARARGS, "(int32 words, min, max) of a ragged corpus"},
+    {"widen_i32", widen_i32, METH_VARARGS, "fresh int64 array (huge pages) of n int32 at an address"},
     {NULL, NULL, 0, NULL}};
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_wdhost", "warpdraw B200 host helpers", -1, methods,
