@@ -341,8 +341,12 @@ inline int launch_rows_lane(const DrawParams<float>& p, cudaStream_t st) {
 }
 
 // The small-K LDA draw (wd_small.cuh): K = 8 * RM + 32 * NB, 2 <= NB <= 8,
-// fp32, W = 32, 256-bit aligned rows.  WD_SMALL_LDA: 0 off, 1 on vocabulary
-// tiles (DeviceLDA's run-padded token order), 2 also on CSR-order draws.
+// fp32, W = 32, 256-bit aligned rows.  WD_SMALL_LDA: 0 off, 1 (default) on
+// vocabulary tiles (DeviceLDA's run-padded token order) and on CSR-order
+// draws up to K = 256, 2 on every eligible draw.  CSR order, 1M documents,
+// general kernel -> small (ms): K = 64 9.91 -> 5.75, 128 12.54 -> 8.55,
+// 200 16.62 -> 12.82, 256 17.35 -> 13.61, 280 22.65 -> 22.61; at 20 tokens
+// per document K = 280 loses (10.1 -> 11.9), hence the cap.
 template <int NB, int RM>
 int launch_small_inst(const DrawParams<float>& p, cudaStream_t st) {
   const void* fn = (const void*)lda_small_kernel<NB, RM>;
@@ -374,7 +378,7 @@ inline bool small_lda_eligible(const DrawParams<float>& p) {
   static int on = env_int("WD_SMALL_LDA", 1);
   const int nb = p.K / 32;
   if (!on || (p.K % 32) % 8 != 0 || nb < 2 || nb > 8) return false;
-  return on == 2 || p.token_pos != nullptr;
+  return on == 2 || p.token_pos != nullptr || p.K <= 256;
 }
 inline int launch_small_lda(const DrawParams<float>& p0, cudaStream_t st) {
   DrawParams<float> p = p0;

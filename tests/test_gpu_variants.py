@@ -6,7 +6,7 @@ setting runs in a child process: the register-lean LDA draw
 (WD_LEAN_MIN_NB=16 takes it down to K = 512, WD_LEAN_COOP=1 its warp-
 cooperative pass 2, WD_LEAN_PF its theta L2 prefetch), the one-row-per-thread
 rows kernel on every shape it supports (WD_ROWS_LANE=2), the small-K LDA
-kernel on CSR-order draws too (WD_SMALL_LDA=2), and all of them disabled
+kernel on every CSR-order draw (WD_SMALL_LDA=2, default K <= 256), and all of them disabled
 (the general kernels on the same shapes)."""
 
 import json
@@ -58,6 +58,9 @@ for K in (72, 200, 256, 512, 1024, 2048):
         z = wd.draw_z_device("butterfly", dc, th, ph, wd.SeededStops(5), 32, tiles=tiles).cpu().numpy()
         exp, err = O.draw_z_csr(theta, phi, off, words, W=32, seed=5, threads=8)
         out["lda"].append([K, pad, int(np.sum(z != exp)), err is None])
+        if pad == 0:  # the CSR-order draw (no tiles) of the same corpus
+            z = wd.draw_z_device("butterfly", dc, th, ph, wd.SeededStops(5), 32).cpu().numpy()
+            out["lda"].append([K, -1, int(np.sum(z != exp)), err is None])
 print(json.dumps(out))
 """
 
