@@ -660,6 +660,9 @@ def _upload_params(x, lanes, slot):
     return buf
 
 
+_ASYNC_OUT_MIN = 1 << 16  # tokens: below this the synchronous path is as fast
+
+
 def _to_host_ragged(z_dev, offsets_host):
     """z (int32, device) -> list of int64 arrays: D2H into a cached pinned
     buffer, widened by torch's multi-threaded copy into one fresh int64
@@ -681,8 +684,42 @@ def _to_host_ragged(z_dev, offsets_host):
     return csr_to_ragged(z64, offsets_host)
 
 
+# Pinned int64 host buffers the reference-signature call returns z in (its
+# per-document arrays are views of one).  An entry is [tensor, weakref to the
+# ndarray handed out]: it is reused once every view of that ndarray is gone
+# (the weakref is dead), so a caller that keeps the previous call's z while
+# making the next call (run_gibbs) alternates between two buffers.  At most
+# _Z_OUT_POOL_MAX buffers; a caller holding more results gets the pageable
+# path (_to_host_ragged).
+_Z_OUT_POOL_MAX = 3
+_z_out_pool: list = []
+
+
+def _z_out_buffer(n):
+    """(pinned int64 tensor, its ndarray) with room for n values and no live
+    views, or None when the pool is full of buffers still referenced."""
+    import weakref
+
+    torch = _torch()
+    free = [e for e in _z_out_pool if e[1] is None or e[1]() is None]
+    ent = next((e for e in free if e[0].numel() >= n), None)
+    if ent is None:
+        if free:  # a free buffer that is too small: replace it
+            _z_out_pool.remove(free[0])
+        elif len(_z_out_pool) >= _Z_OUT_POOL_MAX:
+            return None
+        ent = [torch.empty(max(int(n), 1), dtype=torch.int64).pin_memory(), None]
+        _z_out_pool.append(ent)
+    full = ent[0].numpy()
+    ent[1] = weakref.ref(full)
+    return ent[0], full
+
+
 # wall-clock phases of the last reference-signature call (seconds): corpus
-# lookup/upload, theta+phi upload, draw (incl. its error check), z download
+# lookup/upload, theta+phi upload enqueue, then on the synchronous path the
+# draw (incl. its error check) and the z download; on the pinned-buffer path
+# (large corpora) upload_and_draw is the enqueue of everything plus the
+# host-side views, download the remaining wait for the stream
 last_host_timing: dict = {}
 
 
@@ -709,11 +746,29 @@ def _host_call(kernel, N, theta, phi, w, lanes, stops, trace, threads, step_hook
     keep64 = theta.dtype == np.float32 and phi.dtype == np.float64
     ph = _upload_params(phi if keep64 else phi.astype(theta.dtype, copy=False), lanes, "phi")
     t2 = time.perf_counter()
-    z = draw_z_device(kernel, corpus, th, ph, stops, lanes)  # synchronises (error check)
-    t3 = time.perf_counter()
     off = np.zeros(N.size + 1, dtype=np.int64)
     np.cumsum(N, out=off[1:])
-    out = _to_host_ragged(z, off)
+    n = corpus.n_tokens
+    slot = _z_out_buffer(n) if (n >= _ASYNC_OUT_MIN and _wdhost is not None) else None
+    if slot is None:
+        z = draw_z_device(kernel, corpus, th, ph, stops, lanes)  # synchronises (error check)
+        t3 = time.perf_counter()
+        out = _to_host_ragged(z, off)
+    else:
+        # everything on the stream at once -- uploads, draw, int64 widening,
+        # D2H into the pinned result buffer -- while the host builds the
+        # per-document views of that buffer (they need its address, not its
+        # contents); then one synchronisation and the error check
+        torch = _torch()
+        key_rule = _KERNEL_SPEC[kernel][1]
+        err = torch.empty((1, 2), dtype=torch.int64, device=th.device)
+        z = draw_z_device(kernel, corpus, th, ph, stops, lanes, err=err, check=False)
+        host_t, full = slot
+        host_t[:n].copy_(z.to(torch.int64), non_blocking=True)
+        out = csr_to_ragged(full[:n], off)
+        t3 = time.perf_counter()
+        e = combine_err(err)  # synchronises
+        raise_for_err(e, key_rule, lanes)
     t4 = time.perf_counter()
     last_host_timing.update(corpus=t1 - t0, upload_enqueue=t2 - t1, upload_and_draw=t3 - t1, download=t4 - t3,
                             total=t4 - t0)

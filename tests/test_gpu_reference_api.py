@@ -21,6 +21,7 @@ pytestmark = pytest.mark.gpu
 import paper_1505_03851_b200 as wd  # noqa: E402
 from paper_1505_03851_b200 import _lib  # noqa: E402
 from paper_1505_03851_b200.device_lda import DeviceLDA  # noqa: E402
+from oracle import oracle as O  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -188,3 +189,48 @@ def test_host_corpus_cache_hits_and_invalidates():
     z4 = wd.draw_z("butterfly", N, theta, phi, w, cfg, wd.SeededStops(4))
     for a, b in zip(z3, z4):
         np.testing.assert_array_equal(a, b)
+
+
+def test_large_call_pinned_result_buffers():
+    """Above _ASYNC_OUT_MIN tokens the reference-signature call returns z as
+    views of a pooled pinned buffer: results kept by the caller are never
+    overwritten by later calls (the pool hands out only buffers with no live
+    views, and falls back to fresh memory when all are held), equal the
+    oracle, and an AllZero document still raises after the asynchronous
+    download."""
+    from paper_1505_03851_b200 import kernels as K
+
+    gen = np.random.default_rng(21)
+    M, V, Kt = 2048, 500, 72
+    N = np.maximum(gen.poisson(60, size=M), 1)
+    assert N.sum() >= K._ASYNC_OUT_MIN
+    off = np.concatenate([[0], np.cumsum(N)]).astype(np.int64)
+    flat = gen.integers(0, V, size=int(off[-1]))
+    w = [flat[a:b] for a, b in zip(off[:-1], off[1:])]
+    theta = gen.uniform(0.1, 1, size=(M, Kt)).astype(np.float32)
+    phi = gen.uniform(0.1, 1, size=(V, Kt)).astype(np.float32)
+    cfg = wd.WarpConfig(32, 4)
+    K._z_out_pool.clear()
+    kept = []
+    for seed in range(K._Z_OUT_POOL_MAX + 2):  # more results held than pool buffers
+        z = wd.draw_z("butterfly", N, theta, phi, w, cfg, wd.SeededStops(seed))
+        kept.append((seed, z))
+    assert len(K._z_out_pool) == K._Z_OUT_POOL_MAX
+    for seed, z in kept:
+        exp, err = O.draw_z_csr(theta, phi, off, flat, W=32, seed=seed, threads=8)
+        assert err is None
+        np.testing.assert_array_equal(np.concatenate(z), exp)
+        assert z[0].dtype == np.int64 and len(z) == M
+    # dropping a result frees its buffer for the next call (no new buffer)
+    bufs = [e[0].data_ptr() for e in K._z_out_pool]
+    del kept[1:3]
+    z = wd.draw_z("butterfly", N, theta, phi, w, cfg, wd.SeededStops(99))
+    assert [e[0].data_ptr() for e in K._z_out_pool] == bufs
+    exp, _ = O.draw_z_csr(theta, phi, off, flat, W=32, seed=99, threads=8)
+    np.testing.assert_array_equal(np.concatenate(z), exp)
+    np.testing.assert_array_equal(np.concatenate(kept[0][1]),
+                                  O.draw_z_csr(theta, phi, off, flat, W=32, seed=0, threads=8)[0])
+    # the error check still runs on the asynchronous path
+    theta[777] = 0
+    with pytest.raises(wd.AllZeroError, match=r"^document 777: all products are zero$"):
+        wd.draw_z("butterfly", N, theta, phi, w, cfg, wd.SeededStops(1))
