@@ -2,7 +2,8 @@
 edge cases the reference tests for the draw: an all-zero
 document (AllZeroError with the reference's message, kernels.py:421-425),
 injected and Philox stops, shards with a non-zero doc_base, padded and
-unpadded vocabulary tiles, against the oracle / the host twin."""
+unpadded vocabulary tiles and the untiled CSR-order draw (which takes the
+small-K kernel up to K = 256), against the oracle / the host twin."""
 
 import numpy as np
 import pytest
@@ -28,9 +29,9 @@ def _dev(a):
 
 
 @pytest.mark.parametrize("K", [200, 232, 2048, 4096])
-@pytest.mark.parametrize("pad", [0, 4])
+@pytest.mark.parametrize("pad", [0, 4, None])  # None: the untiled CSR-order draw
 def test_allzero_document(K, pad):
-    gen = np.random.default_rng(K + pad)
+    gen = np.random.default_rng(K + (pad if pad is not None else 7))
     M, V = 256, 300
     N, off, words = _corpus(gen, M, V, 12)
     dead = int(np.flatnonzero(N > 0)[7])
@@ -38,15 +39,16 @@ def test_allzero_document(K, pad):
     theta[dead] = 0
     phi = gen.uniform(0.05, 1, size=(V, K)).astype(np.float32)
     dc = wd.DeviceCorpus.from_csr(off, words.astype(np.int32))
-    tiles = dc.vocab_tiles(64, pad)
+    tiles = None if pad is None else dc.vocab_tiles(64, pad)
     with pytest.raises(wd.AllZeroError, match=rf"^document {dead}: all products are zero$"):
         wd.draw_z_device("butterfly", dc, _dev(theta), _dev(phi), wd.SeededStops(3), 32, tiles=tiles)
     _, err = O.draw_z_csr(theta, phi, off, words, W=32, seed=3)
     assert err is not None and (err >> 40) * 32 + (err & 0xFF) == dead  # the oracle's first dead document
 
 
-@pytest.mark.parametrize("K", [200, 2048])
-def test_injected_philox_and_doc_base(K):
+@pytest.mark.parametrize("K", [72, 200, 256, 2048])
+@pytest.mark.parametrize("tiled", [True, False])
+def test_injected_philox_and_doc_base(K, tiled):
     """A shard starting at global document 96: seeded keys use global ids;
     injected u per token; Philox stops equal their host twin's u."""
     gen = np.random.default_rng(K)
@@ -56,7 +58,7 @@ def test_injected_philox_and_doc_base(K):
     phi = gen.uniform(0.05, 1, size=(V, K)).astype(np.float32)
     base = 96
     dc = wd.DeviceCorpus.from_csr(off, words.astype(np.int32), doc_base=base)
-    tiles = dc.vocab_tiles(80, 4)
+    tiles = dc.vocab_tiles(80, 4) if tiled else None
     th, ph = _dev(theta), _dev(phi)
     # seeded (global document ids in the keys and in doc mod W)
     z = wd.draw_z_device("butterfly", dc, th, ph, wd.SeededStops(9), 32, tiles=tiles).cpu().numpy()
