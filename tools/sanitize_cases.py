@@ -52,6 +52,8 @@ for K in (64, 200, 232, 2048, 4096):
     for pad in (0, 4):
         wd.draw_z_device("butterfly", dc, tha, pha, wd.SeededStops(4), 32, tiles=dc.vocab_tiles(40, pad),
                          word_topic=wt)
+    # the untiled CSR-order draw (small-K kernel up to K = 256)
+    wd.draw_z_device("butterfly", dc, tha, pha, wd.SeededStops(4), 32, word_topic=wt)
     # float32 theta with float64 phi (wd_mixed.cu), all three kernels
     ph64 = torch.from_numpy(gen.uniform(0.1, 1, size=(V, K))).cuda()
     for kern in ("butterfly", "transposed", "basic"):
