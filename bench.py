@@ -70,6 +70,9 @@ def parse():
                     help="--impl reference: skip timing the reference's own Python draw_z_butterfly")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sampler", action="store_true")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: test the N > 1 flow with every rank on one GPU (ranks share cuda:0..n-1 round robin); "
+                         "not a measurement")
     ap.add_argument("--force-dist", action="store_true",
                     help="create the NCCL process group even at world size 1 (exercises the N>1 code path)")
     return ap.parse_args()
@@ -540,6 +543,8 @@ def main():
     import paper_1505_03851_b200 as wd
     from paper_1505_03851_b200.device_lda import DeviceLDA
 
+    if args.dist_backend == "gloo":  # flow test: ranks may share a GPU
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
@@ -551,7 +556,10 @@ def main():
         if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
             os.environ["NCCL_DEBUG"] = "INFO"
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+        else:
+            dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
         pg = dist.group.WORLD
         dist.barrier()  # the communicator exists (and has logged) before any timing
     K, V = args.topics, args.vocab

@@ -122,3 +122,30 @@ def test_bench_nccl_path_world1():
     assert line["roofline"]["bound"] == "l2" and 0 < line["roofline"]["frac"] <= 1.2
     assert line["scaling"] == "strong" and line["tokens_per_step"] == line["tokens_rank0"]
     assert "nranks 1" in r.stderr or "nRanks 1" in r.stderr  # NCCL communicator line (NCCL_DEBUG=INFO)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_bench_multirank_flow_gloo(world):
+    """bench.py --gpus N as the driver launches it (torchrun, N ranks), with
+    the gloo backend so every rank can share the one GPU: the sharded
+    corpus, per-tile count all-reduces, sharded phi resample, max-over-ranks
+    timing and the single JSON line from rank 0 (numbers meaningless: the
+    ranks share a GPU)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", str(world),
+           "--dist-backend", "gloo", "--steps", "2", "--warmup", "3", "--no-cpu", "--no-sampler", "--no-dropin",
+           "--docs", "64000", "--vocab", "40000"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [x for x in r.stdout.strip().splitlines() if x.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == world and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["config"]["parallelism"].startswith(f"dp{world}")
+    assert line["tokens_per_step"] > line["tokens_rank0"] > 0
+    assert line["roofline"]["draw_ms_max_over_ranks"] >= line["roofline"]["draw_ms"] * 0.999
