@@ -12,6 +12,9 @@ After install():
 * warpdraw.lda's own reference to draw_z is rebound, so gibbs_iterate /
   run_gibbs (and `warpdraw lda --kernel ...`) draw on the GPU while keeping
   the reference's numpy resample -- the results stay bit-identical;
+* warpdraw.lda.topic_counts (lda.py:174-182; called by resample_params)
+  counts on the GPU (wd_topic_counts, reusing the draw's cached corpus
+  upload): integer counts, bit-identical, np.add.at's index rules kept;
 * warpdraw.bench.SAMPLERS["binary" | "alias" | "butterfly"] are the GPU
   samplers (bench.py:150-154), bit-identical, and SAMPLERS["prefix"] (the
   butterfly's u stream through a full prefix table) is added;
@@ -70,6 +73,13 @@ def _wrap_errors(fn, ref_kernels, ref_sampling):
     return call
 
 
+def _topic_counts(corpus, z, n_topics):
+    """The reference's topic_counts(corpus, z, n_topics) on the GPU."""
+    from .lda import counts_ragged
+
+    return counts_ragged(corpus.lengths, corpus.words, z, n_topics, corpus.vocab_size)
+
+
 def install(package: str = "warpdraw") -> None:
     """Patch the imported reference package in place (idempotent)."""
     if _saved:
@@ -79,12 +89,13 @@ def install(package: str = "warpdraw") -> None:
     ref_lda = importlib.import_module(package + ".lda")
     ref_bench = importlib.import_module(package + ".bench")
     _saved["kernels"] = (ref_kernels, dict(ref_kernels.KERNELS), ref_kernels.draw_z)
-    _saved["lda"] = (ref_lda, ref_lda.draw_z)
+    _saved["lda"] = (ref_lda, ref_lda.draw_z, ref_lda.topic_counts)
     _saved["bench"] = (ref_bench, dict(ref_bench.SAMPLERS))
     ref_kernels.KERNELS.update({name: _wrap_errors(fn, ref_kernels, ref_sampling) for name, fn in _k.KERNELS.items()})
     gpu_draw_z = _wrap_errors(_k.draw_z, ref_kernels, ref_sampling)
     ref_kernels.draw_z = gpu_draw_z
     ref_lda.draw_z = gpu_draw_z
+    ref_lda.topic_counts = _topic_counts
     ref_bench.SAMPLERS.update({name: _wrap_errors(fn, ref_kernels, ref_sampling) for name, fn in _s.SAMPLERS.items()})
     # the split table / search API: the defining module and the modules that
     # imported the names (bench.py:19, cli.py uses kernels.<name>)
@@ -105,8 +116,9 @@ def uninstall() -> None:
     ref_kernels.KERNELS.clear()
     ref_kernels.KERNELS.update(kernels)
     ref_kernels.draw_z = draw_z
-    ref_lda, lda_draw_z = _saved.pop("lda")
+    ref_lda, lda_draw_z, lda_topic_counts = _saved.pop("lda")
     ref_lda.draw_z = lda_draw_z
+    ref_lda.topic_counts = lda_topic_counts
     ref_bench, samplers = _saved.pop("bench")
     ref_bench.SAMPLERS.clear()
     ref_bench.SAMPLERS.update(samplers)

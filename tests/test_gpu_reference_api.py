@@ -234,3 +234,37 @@ def test_large_call_pinned_result_buffers():
     theta[777] = 0
     with pytest.raises(wd.AllZeroError, match=r"^document 777: all products are zero$"):
         wd.draw_z("butterfly", N, theta, phi, w, cfg, wd.SeededStops(1))
+
+
+def test_topic_counts_through_install_equal_numpy(warpdraw):
+    """warpdraw.lda.topic_counts after install(): the GPU counts equal the
+    reference's own np.add.at counts, including its index rules (negative z
+    wraps, z >= K and word ids >= V raise IndexError)."""
+    from paper_1505_03851_b200 import integrate
+
+    ref = integrate._saved["lda"][2]  # the reference's own topic_counts
+    gpu = warpdraw.lda.topic_counts
+    assert gpu is not ref
+    gen = np.random.default_rng(31)
+    M, V, Kt = 96, 150, 24
+    N = gen.poisson(12, size=M)
+    N[5] = 0
+    w = [gen.integers(0, V, size=int(n)) for n in N]
+    corpus = warpdraw.lda.Corpus(lengths=N.astype(np.int64), words=w, vocab_size=V)
+    z = [gen.integers(0, Kt, size=int(n)) for n in N]
+    z[7] = z[7] - Kt  # negative topics wrap in np.add.at
+    exp_dt, exp_wt = ref(corpus, z, Kt)
+    got_dt, got_wt = gpu(corpus, z, Kt)
+    assert got_dt.dtype == np.int64 and got_wt.dtype == np.int64
+    np.testing.assert_array_equal(got_dt, exp_dt)
+    np.testing.assert_array_equal(got_wt, exp_wt)
+    bad = list(z)
+    bad[3] = bad[3].copy()
+    bad[3][0] = Kt
+    with pytest.raises(IndexError):
+        gpu(corpus, bad, Kt)
+    w_bad = list(w)
+    w_bad[2] = w_bad[2].copy()
+    w_bad[2][0] = V
+    with pytest.raises(IndexError):
+        gpu(warpdraw.lda.Corpus(lengths=corpus.lengths, words=w_bad, vocab_size=V), z, Kt)

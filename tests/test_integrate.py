@@ -42,6 +42,7 @@ def test_install_patches_and_restores(warpdraw):
     from paper_1505_03851_b200 import integrate
 
     orig_draw = warpdraw.kernels.draw_z
+    orig_counts = warpdraw.lda.topic_counts
     orig_kernels = dict(warpdraw.kernels.KERNELS)
     orig_tables = (warpdraw.kernels.build_block_tables, warpdraw.kernels.butterfly_search,
                    warpdraw.bench.build_block_tables, warpdraw.bench.butterfly_search)
@@ -55,6 +56,7 @@ def test_install_patches_and_restores(warpdraw):
         assert warpdraw.bench.butterfly_search is not orig_tables[3]
         assert warpdraw.kernels.draw_z is not orig_draw
         assert warpdraw.lda.draw_z is warpdraw.kernels.draw_z
+        assert warpdraw.lda.topic_counts is not orig_counts  # lda.py:174-182 on the GPU
         assert set(warpdraw.kernels.KERNELS) == {"basic", "transposed", "butterfly"}
         assert all(warpdraw.kernels.KERNELS[k] is not orig_kernels[k] for k in orig_kernels)
         assert "prefix" in warpdraw.bench.SAMPLERS
@@ -64,6 +66,7 @@ def test_install_patches_and_restores(warpdraw):
     finally:
         integrate.uninstall()
     assert warpdraw.kernels.draw_z is orig_draw
+    assert warpdraw.lda.topic_counts is orig_counts
     assert warpdraw.kernels.KERNELS == orig_kernels
     assert (warpdraw.kernels.build_block_tables, warpdraw.kernels.butterfly_search, warpdraw.bench.build_block_tables,
             warpdraw.bench.butterfly_search) == orig_tables
