@@ -25,6 +25,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1505_03851_b200 as wd  # noqa: E402
+from paper_1505_03851_b200.device_lda import RUN_PAD_MIN_MEAN_RUN, lean_draw  # noqa: E402
 
 
 def _graph(body, iters):
@@ -113,19 +114,25 @@ def main():
     for K in [int(x) for x in a.lda_ks.split(",")]:
         # the product's layout (DeviceLDA): line-aligned theta/phi blocks,
         # vocabulary tiles when phi exceeds ~40 MB, and for the butterfly
-        # kernel (tile, document) runs padded to 8 when they are long
+        # kernel the token list (document, word)-ordered in every tile with
+        # (tile, document) runs padded to the 4-row lane groups by
+        # DeviceLDA's rule (device_lda.py); the prefix-table baseline keeps
+        # CSR order unless phi needs tiling
         theta = wd.kernels.to_block_aligned(torch.rand((M, K), generator=g, device="cuda") * 0.9 + 0.1)
         phi = wd.kernels.to_block_aligned(torch.rand((V, K), generator=g, device="cuda") * 0.9 + 0.1)
         r = {"K": K}
-        rows_t = (40 << 20) // (4 * K)
         tiled = V * K * 4 > (40 << 20)
-        n_tiles = -(-V // rows_t) if tiled else 1
-        pad = 8 if (tiled and K // 32 <= 32 and T / M / n_tiles >= 20) else 0
+        rows_t = (40 << 20) // (4 * K) if tiled else V
+        n_tiles = -(-V // rows_t)
+        pad = 4 if (K // 32 <= 32 and T / M / n_tiles >= RUN_PAD_MIN_MEAN_RUN) else 0
+        if lean_draw(K, 32, 4):
+            pad = 4
         r["vocab_tiles"] = n_tiles
         r["run_pad"] = pad
         terr = torch.empty((n_tiles, 2), dtype=torch.int64, device="cuda")
+        bfly_tiles = dc.vocab_tiles(rows_t, pad)
         for kern in ("butterfly", "transposed"):
-            tiles = dc.vocab_tiles(rows_t, pad if kern == "butterfly" else 0) if tiled else None
+            tiles = bfly_tiles if kern == "butterfly" else (dc.vocab_tiles(rows_t, 0) if tiled else None)
             dt = timed(lambda: wd.draw_z_device(kern, dc, theta, phi, wd.SeededStops(3), 32, z=z, err=terr,
                                                 check=False, tiles=tiles), flush, iters=5, warm=2)
             r[kern] = {"ms": dt * 1e3, "tokens_per_s": T / dt,
