@@ -21,8 +21,6 @@ from __future__ import annotations
 
 import os
 
-import numpy as np
-
 from . import _lib
 from .kernels import DeviceCorpus, SeededStops, block_aligned_rows, combine_err, draw_z_device, raise_for_err
 from .rng import derive_seed

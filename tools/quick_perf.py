@@ -1,7 +1,6 @@
 """Quick kernel timing (CUDA events) for development; not the bench contract."""
 import json
 import sys
-import time
 
 import torch
 
