@@ -230,10 +230,21 @@ def test_large_call_pinned_result_buffers():
     np.testing.assert_array_equal(np.concatenate(z), exp)
     np.testing.assert_array_equal(np.concatenate(kept[0][1]),
                                   O.draw_z_csr(theta, phi, off, flat, W=32, seed=0, threads=8)[0])
+    # the other two kernels and injected stops on the same path
+    u = gen.random(int(off[-1]))
+    ragged_u = [u[a:b] for a, b in zip(off[:-1], off[1:])]
+    for kern, variant, rule in (("transposed", O.PREFIX, O.KEY_MASTER), ("basic", O.PREFIX, O.KEY_POSITION)):
+        z = wd.draw_z(kern, N, theta, phi, w, cfg, wd.SeededStops(5))
+        exp, _ = O.draw_z_csr(theta, phi, off, flat, W=32, seed=5, variant=variant, key_rule=rule, threads=8)
+        np.testing.assert_array_equal(np.concatenate(z), exp)
+    z = wd.draw_z("butterfly", N, theta, phi, w, cfg, wd.InjectedStops(ragged_u))
+    np.testing.assert_array_equal(np.concatenate(z), O.draw_z_csr(theta, phi, off, flat, W=32, units_=u, threads=8)[0])
     # the error check still runs on the asynchronous path
     theta[777] = 0
     with pytest.raises(wd.AllZeroError, match=r"^document 777: all products are zero$"):
         wd.draw_z("butterfly", N, theta, phi, w, cfg, wd.SeededStops(1))
+    with pytest.raises(wd.AllZeroError, match=r"^document 777, word 0: all products are zero$"):
+        wd.draw_z("basic", N, theta, phi, w, cfg, wd.SeededStops(1))
 
 
 def test_topic_counts_through_install_equal_numpy(warpdraw):
