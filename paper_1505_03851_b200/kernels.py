@@ -19,6 +19,7 @@ tests/test_gpu_parity.py).  Two entry levels:
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -707,6 +708,15 @@ def _z_out_buffer(n):
         if free:  # a free buffer that is too small: replace it
             _z_out_pool.remove(free[0])
         elif len(_z_out_pool) >= _Z_OUT_POOL_MAX:
+            return None
+        # page-locked memory is taken from the host: keep the pool under a
+        # quarter of physical memory
+        held = sum(e[0].numel() * 8 for e in _z_out_pool)
+        try:
+            phys = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+        except (ValueError, OSError, AttributeError):
+            phys = 0
+        if phys and held + 8 * int(n) > phys // 4:
             return None
         ent = [torch.empty(max(int(n), 1), dtype=torch.int64).pin_memory(), None]
         _z_out_pool.append(ent)
