@@ -675,8 +675,6 @@ def _to_host_ragged(z_dev, offsets_host):
     if _wdhost is not None and hasattr(_wdhost, "widen_i32"):
         # a fresh huge-page mapping filled by several threads (the page
         # faults of a fresh 4K-page buffer cost more than the copy)
-        import os
-
         z64 = _wdhost.widen_i32(pin.data_ptr(), n, max(1, min(16, len(os.sched_getaffinity(0)))))
     else:
         z64 = torch.empty(n, dtype=torch.int64)
