@@ -51,6 +51,14 @@ __device__ __forceinline__ uint4 rand4(const GammaRow& g, uint32_t k, uint32_t c
 // float: the resolution near 0 is 2^-33, so log U reaches -22.9)
 __device__ __forceinline__ float u01(uint32_t x) { return fmaf((float)x, 0x1p-32f, 0x1p-33f); }
 
+// __logf (lg2.approx.ftz times ln2, the same two instructions and bits) as
+// volatile asm, which the compiler may not hoist out of a branch
+__device__ __forceinline__ float logf_unspeculated(float x) {
+  float y;
+  asm volatile("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y * 0.693147182464599609375f;
+}
+
 // One Marsaglia-Tsang attempt (2000) for log Gamma(a, 1) from the counter
 // block (row key, topic, attempt); shapes a < 1 use the boost Gamma(a) = Gamma(a + 1)
 // * U^(1/a) (numpy's construction) with U taken from the same block -- its
@@ -74,11 +82,13 @@ __device__ __forceinline__ bool log_gamma_attempt(float a, const GammaRow& g, ui
   v = v * v * v;
   const float u = u01(r.z);
   const float x2 = x * x;
-  if (u < 1.f - 0.0331f * x2 * x2 || __logf(u) < 0.5f * x2 + d * (1.f - v + __logf(v))) {
-    out = __logf(d * v) + boost;
-    return true;
-  }
-  return false;
+  // the squeeze accepts ~98% of attempts; the exact test's two logs run only
+  // when it fails (volatile: ptxas would otherwise evaluate them for every
+  // attempt -- the same values, so the same decisions, either way)
+  bool ok = u < 1.f - 0.0331f * x2 * x2;
+  if (!ok) ok = logf_unspeculated(u) < 0.5f * x2 + d * (1.f - v + logf_unspeculated(v));
+  if (ok) out = __logf(d * v) + boost;
+  return ok;
 }
 
 // Shapes below kSmallShape (the zero-count cells of theta: alpha = 0.1):
