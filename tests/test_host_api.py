@@ -239,3 +239,29 @@ def test_host_helper_ragged_loops_match_numpy():
     views2[7] = views2[7].copy()
     assert not K._wdhost.ids_equal(views2, ids)
     assert not K._wdhost.ids_equal(views[:-1], ids)
+
+
+def test_flat_topics_follows_np_add_at_index_rules():
+    """The GPU topic_counts' host-side flattening of a ragged z: CSR order,
+    each document's first `length` entries, negative topics wrapped as
+    np.add.at wraps them, out-of-range topics rejected with IndexError --
+    with the native helper and through the numpy path alike."""
+    from paper_1505_03851_b200 import kernels as Kmod
+    from paper_1505_03851_b200.lda import _flat_topics
+
+    K = 7
+    z = [np.array([0, 6, -1]), np.array([], dtype=np.int64), np.array([-7, 3], dtype=np.int32)]
+    lengths = np.array([3, 0, 2], dtype=np.int64)
+    exp = np.array([0, 6, 6, 0, 3], dtype=np.int32)
+    np.testing.assert_array_equal(_flat_topics(z, lengths, K), exp)
+    saved = Kmod._wdhost
+    try:
+        Kmod._wdhost = None  # the numpy path
+        np.testing.assert_array_equal(_flat_topics(z, lengths, K), exp)
+        with pytest.raises(IndexError, match="out of bounds"):
+            _flat_topics([np.array([7])], np.array([1]), K)
+    finally:
+        Kmod._wdhost = saved
+    for bad in (7, -8, 1 << 40):
+        with pytest.raises(IndexError, match="out of bounds"):
+            _flat_topics([np.array([1, bad])], np.array([2]), K)
