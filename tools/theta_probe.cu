@@ -173,6 +173,76 @@ __global__ void __launch_bounds__(128, 8) probe_ring(const float* __restrict__ p
   if (acc == 1234.5f) out[0] = acc;
 }
 
+// theta from shared memory (TS = 1: two LDS.128 per block from a per-warp
+// tile holding 16 blocks of the chunk's two documents' rows, the lane group's
+// document selecting the half; TS = 2: no theta load at all, a register
+// constant) -- what the L1 data pipe charges for the theta operand
+template <int TS>
+__global__ void __launch_bounds__(128, 8) probe_smem(const float* __restrict__ phi, const int* __restrict__ rows,
+                                                     int n_chunks, float* out, const float* __restrict__ theta_g) {
+  __shared__ __align__(16) float tile[4][2][16][32];  // [warp][doc][block mod 16][topic]
+  const int lane = threadIdx.x & 31, s = lane & 3, rg = lane >> 2, wib = threadIdx.x >> 5;
+  const int wpb = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < 4 * 2 * 16 * 32; i += blockDim.x) (&tile[0][0][0][0])[i] = 1.f + (i & 7);
+  __syncthreads();
+  float acc = 0.f;
+  const int cs = gridDim.x * wpb;
+  const float* tw = &tile[wib][rg >> 2][0][s * 8];
+  for (int c = blockIdx.x * wpb + wib; c < n_chunks; c += cs) {
+    const int my = rows[c * 32 + lane];
+    uint32_t r[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) r[kk] = __shfl_sync(FULL, my, rg * 4 + kk);
+    float run = 0.f;
+#pragma unroll 2
+    for (int b = 0; b < K / 32; ++b) {
+      float x[4][8], t[8];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) ld_v8(x[kk], phi + (size_t)r[kk] * K + b * 32 + s * 8);
+      if (TS == 3) {  // theta LDG by the two leader lane groups only (8 lanes), others a constant
+        if ((rg & 3) == 0) ld_v8(t, theta_g + (size_t)((2 * c + (rg >> 2)) & 1023) * K + b * 32 + s * 8);
+        else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) t[e] = 1.f + e;
+        }
+      } else if (TS == 4) {  // leader lanes load, store to smem, all lanes read back (broadcast)
+        float* slot = &tile[wib][rg >> 2][b & 15][s * 8];
+        if ((rg & 3) == 0) {
+          float u8[8];
+          ld_v8(u8, theta_g + (size_t)((2 * c + (rg >> 2)) & 1023) * K + b * 32 + s * 8);
+          *reinterpret_cast<float4*>(slot) = make_float4(u8[0], u8[1], u8[2], u8[3]);
+          *reinterpret_cast<float4*>(slot + 4) = make_float4(u8[4], u8[5], u8[6], u8[7]);
+        }
+        __syncwarp();
+        const float4 t0 = *reinterpret_cast<const float4*>(slot);
+        const float4 t1 = *reinterpret_cast<const float4*>(slot + 4);
+        t[0] = t0.x; t[1] = t0.y; t[2] = t0.z; t[3] = t0.w; t[4] = t1.x; t[5] = t1.y; t[6] = t1.z; t[7] = t1.w;
+      } else if (TS == 1) {
+        const float4 t0 = *reinterpret_cast<const float4*>(tw + (b & 15) * 32);
+        const float4 t1 = *reinterpret_cast<const float4*>(tw + (b & 15) * 32 + 4);
+        t[0] = t0.x; t[1] = t0.y; t[2] = t0.z; t[3] = t0.w; t[4] = t1.x; t[5] = t1.y; t[6] = t1.z; t[7] = t1.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) t[e] = 1.f + e + (float)(b & 1);
+      }
+      float q[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        float a = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a += x[kk][e] * t[e];
+        q[kk] = a;
+      }
+      float v = (s & 1) ? q[1] + __shfl_xor_sync(FULL, q[0], 1) : q[0] + __shfl_xor_sync(FULL, q[1], 1);
+      float w = (s & 1) ? q[3] + __shfl_xor_sync(FULL, q[2], 1) : q[2] + __shfl_xor_sync(FULL, q[3], 1);
+      float z = (s & 2) ? w + __shfl_xor_sync(FULL, v, 2) : v + __shfl_xor_sync(FULL, w, 2);
+      run += z;
+    }
+    acc += run;
+  }
+  if (acc == 1234.5f) out[0] = acc;
+}
+
 int main(int argc, char** argv) {
   const int n_chunks = argc > 1 ? atoi(argv[1]) : 131072;
   const int vrows = argc > 2 ? atoi(argv[2]) * 64 : 2560;  // phi slice, MB (default 40)
@@ -212,7 +282,18 @@ int main(int argc, char** argv) {
   };
   const int grid = sms * 8;
 #define RUN(NAME, ...) timeit(NAME, [&] { probe<__VA_ARGS__><<<grid, 128>>>(phi, theta, rows, n_chunks, n_theta, out); })
-  if (argc > 3) {  // short list
+  if (argc > 3 && argv[3][0] == 's') {  // theta operand source
+    RUN("resident (theta LDG, L2)", 0, false, 0, false);
+    timeit("theta from smem (2x LDS.128)", [&] { probe_smem<1><<<grid, 128>>>(phi, rows, n_chunks, out, theta); });
+    timeit("no theta load", [&] { probe_smem<2><<<grid, 128>>>(phi, rows, n_chunks, out, theta); });
+    timeit("theta LDG by leader lanes", [&] { probe_smem<3><<<grid, 128>>>(phi, rows, n_chunks, out, theta); });
+    timeit("leader LDG + smem bcast", [&] { probe_smem<4><<<grid, 128>>>(phi, rows, n_chunks, out, theta); });
+    RUN("resident (theta LDG, L2)", 0, false, 0, false);
+    timeit("theta from smem (2x LDS.128)", [&] { probe_smem<1><<<grid, 128>>>(phi, rows, n_chunks, out, theta); });
+    timeit("no theta load", [&] { probe_smem<2><<<grid, 128>>>(phi, rows, n_chunks, out, theta); });
+    timeit("theta LDG by leader lanes", [&] { probe_smem<3><<<grid, 128>>>(phi, rows, n_chunks, out, theta); });
+    timeit("leader LDG + smem bcast", [&] { probe_smem<4><<<grid, 128>>>(phi, rows, n_chunks, out, theta); });
+  } else if (argc > 3) {  // short list
     RUN("resident", 0, false, 0, false);
     RUN("stream", 1, false, 0, false);
     RUN("stream+ef", 1, true, 0, false);
