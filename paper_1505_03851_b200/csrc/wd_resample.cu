@@ -378,14 +378,35 @@ __global__ void __launch_bounds__(kPhiThreads) phi_pass(int pass, const int32_t*
         }
       }
     }
-    for (int64_t v = v0; v < v1 && pass > 0; ++v) {
-      T* p = phi + v * ld + k;
-      if (pass == 1) {
-        const float e = __expf((float)*p - cs);
-        *p = (T)e;
-        acc += e;
-      } else {
-        *p = (T)((float)*p / cs);
+    if (pass > 0) {
+      // four rows' loads in flight before their arithmetic (the column sum
+      // keeps its row order: the same bits as one row at a time)
+      int64_t v = v0;
+      for (; v + 4 <= v1; v += 4) {
+        T* p = phi + v * ld + k;
+        float x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = (float)p[i * ld];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (pass == 1) {
+            const float e = __expf(x[i] - cs);
+            p[i * ld] = (T)e;
+            acc += e;
+          } else {
+            p[i * ld] = (T)(x[i] / cs);
+          }
+        }
+      }
+      for (; v < v1; ++v) {
+        T* p = phi + v * ld + k;
+        if (pass == 1) {
+          const float e = __expf((float)*p - cs);
+          *p = (T)e;
+          acc += e;
+        } else {
+          *p = (T)((float)*p / cs);
+        }
       }
     }
     if (pass < 2) part[g * K + k] = acc;
