@@ -321,3 +321,44 @@ def test_device_chain_matches_reference_chain_at_cfg3_scale():
     crit = f_dist.ppf(0.999, K - 1, K - 1)
     assert chi_dev / chi_alt < crit, (chi_dev, chi_alt, crit)
     assert chi_alt / chi_dev < crit, (chi_dev, chi_alt, crit)
+
+
+@pytest.mark.parametrize("dtype,lanes", [("float64", 32), ("float32", 16), ("float64", 8)])
+def test_device_lda_other_dtypes_and_lane_counts(dtype, lanes):
+    """DeviceLDA beyond fp32 / W = 32 (the general kernels, theta_kernel<double>,
+    phi_pass<double>, vocabulary tiles with W / 4 run padding): each
+    iteration's z equals the oracle's draw on the iteration's own theta /
+    phi, the fused counts equal the oracle's counts, theta rows and phi
+    columns are distributions, and the log-likelihood rises."""
+    from oracle import oracle as O
+
+    tdt = getattr(torch, dtype)
+    gen = np.random.default_rng(lanes)
+    M, V, K = 256, 500, 48
+    N = np.maximum(gen.poisson(30, size=M), 0)
+    off = np.concatenate([[0], np.cumsum(N)]).astype(np.int64)
+    words = gen.integers(0, V, size=int(off[-1])).astype(np.int32)
+    dc = wd.DeviceCorpus.from_csr(off, words)
+    lda = DeviceLDA(dc, K, V, lanes=lanes, dtype=tdt, seed=11, vocab_tile_bytes=100 * K * tdt.itemsize)
+    assert lda.tiles.n_tiles == 5
+    lda.init_from_assignments()
+    ll0 = lda.log_likelihood()
+    for t in range(4):
+        theta = lda.theta.cpu().numpy()
+        phi = lda.phi.cpu().numpy()
+        lda.draw(t)
+        torch.cuda.synchronize()
+        lda.check_errors()
+        exp, err = O.draw_z_csr(theta, phi, off, words, W=lanes, seed=wd.derive_seed(11, 1, t), threads=8)
+        assert err is None
+        np.testing.assert_array_equal(lda.z.cpu().numpy(), exp)
+        dt_o, wt_o = O.topic_counts(off, words, exp, K, V)
+        np.testing.assert_array_equal(lda.word_topic.cpu().numpy(), wt_o)
+        lda.resample(t)
+    torch.cuda.synchronize()
+    th = lda.theta.cpu().numpy()
+    ph = lda.phi.cpu().numpy()
+    assert th.dtype == np.dtype(dtype) and ph.dtype == np.dtype(dtype)
+    np.testing.assert_allclose(th.sum(1), 1.0, rtol=1e-4)
+    np.testing.assert_allclose(ph.sum(0), 1.0, rtol=1e-4)
+    assert lda.log_likelihood() > ll0
