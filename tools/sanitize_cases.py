@@ -92,5 +92,14 @@ lda = DeviceLDA(wd.DeviceCorpus.from_csr(off, words), K, V, seed=1)
 lda.init_from_assignments()
 lda.iterate(0)
 lda.log_likelihood()
+# phi resample with several rows per chunk (the 4-row loop and its tail):
+# V = 5000 over the fixed row chunks, fp32 and fp64
+for dt in (torch.float32, torch.float64):
+    V, K = 5000, 40
+    wt = torch.randint(0, 5, (V, K), dtype=torch.int32, device="cuda")
+    ph = torch.empty((V, K), dtype=dt, device="cuda")
+    ws = torch.empty(int(L.wd_resample_phi_workspace_bytes(K)), dtype=torch.uint8, device="cuda")
+    _lib.check(L.wd_resample_phi(_lib.WD_FLOAT32 if dt == torch.float32 else _lib.WD_FLOAT64, wt.data_ptr(), V, K,
+                                 0.01, 3, ph.data_ptr(), K, ws.data_ptr(), ws.numel(), _lib.stream_handle()), "phi")
 torch.cuda.synchronize()
 print("sanitize cases done")
